@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the FHT2D merge DP (arXiv 2411.07351) on B200.
+
+Contract:
+  python bench.py --gpus N --steps K --warmup W [--config c4] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch of the workload (default
+config c4: 256 binary 509x509 edge maps, all four quadrants, u8 -> int32).
+Each rank processes its own 256-image shard (weak scaling; no collective on
+the data path).  `value` is whole-job FHT Gsums/s (BASELINE.json metric:
+Q * images * n^2 * ceil(log2 n) nominal adds / s) with inputs resident in HBM;
+`e2e` is the same metric through the C-ABI host-buffer call
+(fht_execute_host: H2D of the inputs + transform + D2H of every Hough image).
+Between timed steps L2 is flushed (a 512 MiB write, untimed); each step is
+timed with CUDA events on the launching stream; the max over ranks is taken.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2411_07351_b200 import fht, workloads  # noqa: E402
+from paper_2411_07351_b200._lib import check, lib  # noqa: E402
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strategy", default="tweaked", choices=["simple", "tweaked"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        p = json.loads(PEAKS_FILE.read_text())
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_baseline(cfg: str, strategy: int, seconds: float, threads: int | None = None):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference library, fht::fht2d_quadrants / fht2d_counted) on this host,
+    images across `threads` host threads, on a bounded sample of the workload.
+    Falls back to the C restatement (oracle/liboracle.so) if _ref is absent."""
+    import oracle
+
+    c = workloads.CONFIGS[cfg]
+    threads = threads or oracle.host_threads()
+    kind = "reference" if oracle.ref_available() else "port"
+    quads = c.quadrants if c.n < 3000 else ("horiz_pos",)  # bound one sample of the big configs to one quadrant
+    mask = sum(1 << workloads.ALL_Q.index(q) for q in quads)
+    if c.dtype == "u8":
+        per = max(1, min(threads, c.batch))
+        imgs = workloads.make_images(cfg, per)
+        proxy = ""
+    else:
+        # The reference has no float path: time its int64 path on
+        # a same-size integer image ("int64 proxy": same add tree, 8-byte cells).
+        per = 1
+        imgs = np.random.default_rng(0).integers(0, 256, (1, c.n, c.n), dtype=np.uint8)
+        proxy = " (int64 proxy: reference has no float path)"
+    fn = oracle.ref_batch_quadrants_u8 if kind == "reference" else oracle.batch_quadrants_u8_port
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        fn(imgs, strategy, threads=threads, mask=mask)
+        done += per
+        if time.perf_counter() - t0 >= seconds or done >= 64 * per:
+            break
+    dt = time.perf_counter() - t0
+    sums = len(quads) * done * c.n * c.n * int(np.ceil(np.log2(c.n)))
+    return {"value": sums / dt / 1e9, "unit": "Gsums/s", "cores": threads, "kind": kind,
+            "sample": f"{done} image(s) of {cfg} ({c.n}x{c.n}, {len(quads)} quadrant(s)){proxy}, "
+                      f"{dt:.2f} s on {threads} host thread(s)"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+
+    c = workloads.CONFIGS[args.config]
+    strategy = 0 if args.strategy == "simple" else 1
+    threads = oracle.host_threads()
+    for _ in range(args.warmup):
+        cpu_baseline(args.config, strategy, 0.0, threads)
+    per_step = []
+    vals = []
+    for _ in range(args.steps):
+        r = cpu_baseline(args.config, strategy, 0.0, threads)
+        vals.append(r["value"])
+        per_step.append(r)
+    value = statistics.median(vals)
+    sample = per_step[-1]
+    line = {
+        "impl": "reference", "metric": "FHT Gsums/s", "value": value, "unit": "Gsums/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.config, "description": c.description, "strategy": args.strategy},
+        "cpu_baseline": {"value": value, "unit": "Gsums/s", "cores": sample["cores"], "kind": sample["kind"],
+                         "sample": sample["sample"]},
+        "e2e": {"value": value, "unit": "Gsums/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+ESZ = {"u8": 1, "i32": 4, "i64": 8, "f32": 4}
+
+
+def algorithmic_bytes(plan: fht.Plan, c: workloads.Config, kind: int, nops: int, W: int, H: int, slots: int):
+    """each distinct input cell read once, each output cell
+    written once, per launch.  K1: W*H*(e_in + e_acc); K2/K3: nops*H*2*e_acc."""
+    ea = ESZ[c.acc]
+    if kind == 1:
+        return slots * W * H * (ESZ[c.dtype] + ea)
+    return slots * nops * H * 2 * ea
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = workloads.CONFIGS[args.config]
+    strategy = 0 if args.strategy == "simple" else 1
+
+    imgs = workloads.make_images(args.config, c.batch, offset=rank * c.batch)  # this rank's shard
+    plan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=list(c.quadrants),
+                    batch=c.batch, device=local)
+    x = torch.from_numpy(imgs).to(dev)
+    out = plan.alloc_outputs()
+    wsbuf = plan.workspace()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    cells = c.n * c.n
+
+    ptrs = (ctypes.c_void_p * 4)()
+    for i, q in enumerate(fht.QUADRANTS):
+        ptrs[i] = out[q].data_ptr() if q in out else None
+
+    def step():
+        check(lib().fht_execute(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
+                                ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
+                                ctypes.c_void_p(stream.cuda_stream)))
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s, e in evs:
+        flush.fill_(1)  # L2 flush, outside the timed interval
+        s.record(stream)
+        step()
+        e.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    total_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    sums_per_step = workloads.nominal_sums(args.config) * ws
+    value = sums_per_step / (ms_per_step * 1e-3) / 1e9
+
+    # Per-kernel live timing (events between launches, same stream) for the roofline.
+    desc = plan.describe()
+    nl = plan.launches
+    ms_arr = (ctypes.c_float * nl)()
+    kind_arr = (ctypes.c_int * nl)()
+    got = ctypes.c_int()
+    per_launch = []
+    for _ in range(3):
+        flush.fill_(1)
+        check(lib().fht_execute_profiled(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
+                                         ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
+                                         ctypes.c_void_p(stream.cuda_stream), ms_arr, kind_arr, nl, ctypes.byref(got)))
+        per_launch.append(list(ms_arr)[:got.value])
+    kinds = list(kind_arr)[:got.value]
+    med = [statistics.median(v) for v in zip(*per_launch)]
+    # Map each launch to its byte count.
+    g = desc["groups"][0]
+    sp = g["plan"]
+    slots_total = c.batch * len(g["quadrants"])
+    chunk_slots = desc["chunk"] * len(g["quadrants"])
+    launch_bytes = []
+    lvl_nops = [lv["ops"] for lv in sp["levels"]]
+    k = 0
+    for img0 in range(0, c.batch, desc["chunk"]):
+        nimg = min(desc["chunk"], c.batch - img0)
+        slots = nimg * len(g["quadrants"])
+        launch_bytes.append(algorithmic_bytes(plan, c, 1, 0, sp["W"], sp["H"], slots))
+        if not sp["root_is_block"]:
+            for nops in lvl_nops:
+                launch_bytes.append(algorithmic_bytes(plan, c, 2, nops, sp["W"], sp["H"], slots))
+    by_kind: dict[int, list] = {}
+    for kd, ms, b in zip(kinds, med, launch_bytes):
+        by_kind.setdefault(kd, []).append((ms, b))
+    names = {1: "k1_blocks", 2: "k2_level", 3: "k3_root"}
+    kernel_share = {names[kd]: sum(m for m, _ in v) for kd, v in by_kind.items()}
+    dom = max(by_kind, key=lambda kd: sum(m for m, _ in by_kind[kd]))
+    dom_ms = statistics.mean(m for m, _ in by_kind[dom])
+    dom_bytes = statistics.mean(b for _, b in by_kind[dom])
+    peak, peak_src = hbm_peak()
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    total_bytes = sum(launch_bytes)
+    step_gbs = total_bytes / (sum(med) * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(dom_bytes), "avg_launch_ms": round(dom_ms, 5),
+                "step_algorithmic_bytes": int(total_bytes), "step_gbs": round(step_gbs, 1),
+                "kernel_ms": {k2: round(v, 4) for k2, v in kernel_share.items()}}
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            tr = json.loads(prof.read_text()).get(args.config, {}).get(names[dom])
+            if tr:
+                roofline["traffic"] = tr
+        except Exception:
+            pass
+
+    # e2e through the C-ABI host-buffer call (pinned host memory).
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(imgs).pin_memory()
+        h_out = {q: torch.empty(out[q].shape, dtype=out[q].dtype).pin_memory() for q in out}
+        optrs = [h_out[q].data_ptr() if q in h_out else None for q in fht.QUADRANTS]
+        st = torch.cuda.Stream(dev)
+        for _ in range(2):
+            plan.execute_host_ptrs(h_in.data_ptr(), optrs, st.cuda_stream)
+        n_e2e = max(3, min(args.steps, 10))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            plan.execute_host_ptrs(h_in.data_ptr(), optrs, st.cuda_stream)  # synchronises its stream
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
+        e2e = {"value": sums_per_step / e2e_s / 1e9, "unit": "Gsums/s",
+               "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()),
+               "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in h_out.values())),
+               "ms_per_step": round(e2e_s * 1e3, 3), "call": "fht_execute_host (C ABI, pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, strategy, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "FHT Gsums/s", "value": round(value, 3), "unit": "Gsums/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": c.acc,
+            "data": "synthetic (seeded, BASELINE.json config shapes/distributions)",
+            "config": {"workload": args.config, "description": c.description, "n": c.n,
+                       "images_per_gpu": c.batch, "quadrants": len(c.quadrants), "strategy": args.strategy,
+                       "in_dtype": c.dtype, "acc_dtype": c.acc, "parallelism": f"batch-shard x{ws}",
+                       "l2": "flushed between timed steps (512 MiB write, untimed)"},
+            "images_per_s": round(c.batch * ws / (ms_per_step * 1e-3), 1),
+            "hbm_gbs_step": round(step_gbs, 1),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": plan.launches * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/*
+ * fht_b200.h -- C ABI of the B200 (sm_100a) FHT2D merge-DP library
+ * (paper_2411_07351_b200/libfht_b200.so).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * No exception crosses it either: every call returns an FHT_* status and
+ * fht_last_error() holds the message for the calling thread.
+ *
+ * The reference (arXiv 2411.07351 artefact, /root/reference/proj) exposes the
+ * path as C++ free functions in namespace fht; each entry point below names
+ * the one it replaces.  include/fht_b200/fht.hpp rebuilds that exact C++
+ * interface on top of this ABI.
+ *
+ * Layouts.  Images are row-major, x fastest: img[y*width + x]
+ * (image.hpp:13-14, 55-58).  A quadrant's Hough image is in the reference
+ * layout hough[s*W + t] (transform.cpp:80-83; W = working width = image
+ * width for horiz_*, image height for vert_*), or, with FHT_LAYOUT_NATIVE,
+ * slope-major hough[t*H + s].
+ */
+#ifndef FHT_B200_H
+#define FHT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  FHT_ERR_INVALID <-> std::invalid_argument (transform.cpp:63,
+ * split.hpp:34,41,54-55, image.hpp:49-53); FHT_ERR_OVERFLOW <->
+ * std::overflow_error (transform.cpp:24-26). */
+enum {
+    FHT_OK = 0,
+    FHT_ERR_INVALID = 1,
+    FHT_ERR_OVERFLOW = 2,
+    FHT_ERR_CUDA = 3,
+    FHT_ERR_NOMEM = 4,
+    FHT_ERR_INTERNAL = 5
+};
+
+/* SplitStrategy (split.hpp:12-15). */
+enum { FHT_SPLIT_SIMPLE = 0, FHT_SPLIT_TWEAKED = 1 };
+
+/* Element types. */
+enum { FHT_U8 = 0, FHT_I32 = 1, FHT_I64 = 2, FHT_F32 = 3 };
+
+/* Quadrant bits, QuadrantSet order (quadrants.hpp:15-28). */
+enum {
+    FHT_HORIZ_POS = 1, /* fht2d(I)                       */
+    FHT_HORIZ_NEG = 2, /* fht2d(flip_horizontal(I))      */
+    FHT_VERT_POS = 4,  /* fht2d(transpose(I))            */
+    FHT_VERT_NEG = 8,  /* fht2d(flip_horizontal(transpose(I))) */
+    FHT_ALL_QUADRANTS = 15
+};
+
+/* Plan flags. */
+enum {
+    FHT_LAYOUT_REFERENCE = 0, /* hough[s*W + t] */
+    FHT_LAYOUT_NATIVE = 1     /* hough[t*H + s] */
+};
+
+typedef struct fht_plan_s* fht_plan_t;
+
+/* Build the integer-exact split/rounding tables for one (size, strategy)
+ * once and upload them to `device`.  Valid (in, acc, out) type triples:
+ *   (u8|i32, i32, i32)  (u8|i32|i64, i32, i64)  (u8|i32|i64, i64, i64)
+ *   (f32|u8, f32, f32)
+ * An i32 accumulator for u8 input requires W*255 < 2^31 (else
+ * FHT_ERR_OVERFLOW).  `batch` images are processed per execute.  The plan is
+ * immutable after creation and may be shared by host threads.
+ * Replaces the per-call scratch set-up of fht::fht2d_counted
+ * (transform.cpp:62-78). */
+int fht_plan_create(int width, int height, int strategy, int in_dtype, int acc_dtype, int out_dtype,
+                    int quadrant_mask, int batch, int layout, int device, fht_plan_t* plan);
+int fht_plan_destroy(fht_plan_t plan);
+
+/* Device workspace bytes fht_execute needs (two ping-pong buffers per
+ * in-flight (image, quadrant) slot, the reference's out/tmp pair,
+ * transform.cpp:75-76). */
+size_t fht_workspace_bytes(fht_plan_t plan);
+
+/* Merge additions one execute performs: count_additions_tree (oracle.cpp:27-33)
+ * summed over the selected quadrants and the batch, exactly the count
+ * fht2d_counted / fht2d_quadrants report (transform.cpp:56, quadrants.cpp:31). */
+uint64_t fht_additions(fht_plan_t plan);
+
+/* Kernel launches one execute issues (for the bench's gpu_launches). */
+int fht_launches_per_execute(fht_plan_t plan);
+
+/* JSON description of the schedule (blocks, halos, levels). */
+int fht_plan_describe(fht_plan_t plan, char* buf, size_t len);
+
+/* Run the transform of `batch` images on `stream` (a cudaStream_t; NULL =
+ * legacy default stream).  d_in: device pointer, image i at
+ * d_in + i*in_image_stride elements.  d_out[q] for quadrant bit q set in the
+ * plan's mask (others ignored), image i at d_out[q] + i*out_image_stride.
+ * d_workspace: fht_workspace_bytes(plan) bytes of device memory.  Stream
+ * ordered, asynchronous, no host synchronisation.  No overflow check: use
+ * fht_check_budget for non-u8 integer inputs.
+ * Replaces fht::fht2d_quadrants (quadrants.hpp:32, quadrants.cpp:23-41) and,
+ * with a single-quadrant mask, fht::fht2d (transform.hpp:36). */
+int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
+                int64_t out_image_stride, void* d_workspace, void* stream);
+
+/* fht_execute with a CUDA event recorded after every kernel launch on
+ * `stream`; synchronises and returns each launch's duration (ms) and kind
+ * (1 = K1 blocks, 2 = K2 upper level, 3 = K3 root+transpose).  For the
+ * bench's live per-kernel roofline. */
+int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
+                         int64_t out_image_stride, void* d_workspace, void* stream, float* launch_ms,
+                         int* launch_kind, int max_launches, int* n_launches);
+
+/* Same, with HOST buffers: copies the inputs host->device, runs, copies the
+ * outputs device->host and synchronises `stream`.  Uses device staging
+ * buffers owned by the plan (serialised by a per-plan mutex).  Images and
+ * outputs are dense (strides = one image). */
+int fht_execute_host(fht_plan_t plan, const void* h_in, void* const h_out[4], void* stream);
+
+/* check_overflow_budget (transform.cpp:16-27) on device data: *ok_for_i32 =
+ * (width * max|v| < 2^31), returns FHT_ERR_OVERFLOW if width * max|v| >= 2^62.
+ * Synchronises `stream`. */
+int fht_check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok_for_i32, void* stream);
+
+/* The reference entry points with host int64 buffers, bit-exact:
+ *   fht_fht2d_counted_i64  <-> fht::fht2d_counted (transform.hpp:40)
+ *   fht_fht2d_quadrants_i64 <-> fht::fht2d_quadrants (quadrants.hpp:32-33)
+ * The overflow budget is checked on the device (FHT_ERR_OVERFLOW as the
+ * reference's overflow_error); accumulation is int32 when
+ * width * max|v| < 2^31 and int64 otherwise.  Plans are cached per device. */
+int fht_fht2d_counted_i64(const int64_t* img, int width, int height, int strategy, int64_t* hough,
+                          uint64_t* additions);
+int fht_fht2d_quadrants_i64(const int64_t* img, int width, int height, int strategy, int64_t* horiz_pos,
+                            int64_t* horiz_neg, int64_t* vert_pos, int64_t* vert_neg,
+                            uint64_t* total_additions);
+
+/* Host helpers, identical to the reference's integer rules. */
+int fht_split_width(int w, int strategy, int* w0, int* w1);                 /* split.hpp:46-48 */
+int fht_round_half_up_ratio(int64_t num, int64_t den, int64_t* result);     /* split.hpp:53-57 */
+int fht_count_additions_tree(int w, int h, int strategy, uint64_t* result); /* oracle.cpp:27-33 */
+
+/* Host-only export of the schedule tables for one working orientation
+ * (W slopes x H shifts) as JSON: blocks [x0, shape, depth], shapes {width,
+ * steps, halo, step_offset, ops [dst, a, b, shift, extra]} and upper levels
+ * {depth, ops [dst, a, b, r]}.  Needs no GPU; used by the CPU tests that
+ * replay the schedule against the oracle.  Returns FHT_ERR_INVALID if `len`
+ * is too small (then *needed holds the size). */
+int fht_schedule_json(int W, int H, int strategy, int block_width, char* buf, size_t len, size_t* needed);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* fht_last_error(void);
+
+/* Library version string. */
+const char* fht_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FHT_B200_H */

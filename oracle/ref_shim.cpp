@@ -1,0 +1,175 @@
+// ref_shim.cpp -- extern "C" shim over the UNMODIFIED reference library.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file
+// together with the reference sources where they lie under
+// /root/reference/proj/src (transform.cpp, quadrants.cpp, pattern.cpp,
+// oracle.cpp) into oracle/_ref/libfhtref.so.  Nothing is copied: the shim
+// only converts plain pointers into fht::Image values and calls the
+// reference's own public API:
+//   fht::fht2d_counted     transform.hpp:40   (transform.cpp:62-85)
+//   fht::fht2d_quadrants   quadrants.hpp:32   (quadrants.cpp:23-41)
+//   fht::slow_hough        oracle.hpp:17      (oracle.cpp:9-25)
+//   fht::fht2d_pattern     pattern.hpp:20     (pattern.cpp:24-30)
+//   fht::count_additions_tree oracle.hpp:22   (oracle.cpp:27-33)
+// Exceptions are mapped to status codes: 1 invalid_argument, 2
+// overflow_error, 4 anything else; the message goes to `err`.
+//
+// ref_batch_quadrants_u8 is the CPU baseline used by bench.py: it runs the
+// reference fht2d_quadrants on a batch of uint8 images with a pool of host
+// threads (images across threads; the reference is safe to call
+// concurrently).
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fht/oracle.hpp"
+#include "fht/pattern.hpp"
+#include "fht/quadrants.hpp"
+#include "fht/transform.hpp"
+
+namespace {
+
+void set_err(char* err, int errlen, const char* what) {
+    if (!err || errlen <= 0) return;
+    std::strncpy(err, what, static_cast<std::size_t>(errlen - 1));
+    err[errlen - 1] = '\0';
+}
+
+template <class F>
+int guarded(char* err, int errlen, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    } catch (const std::overflow_error& e) {
+        set_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 4;
+    }
+}
+
+fht::SplitStrategy strat(int s) { return s == 0 ? fht::SplitStrategy::Simple : fht::SplitStrategy::Tweaked; }
+
+void copy_out(const fht::HoughImage& h, int64_t* out) {
+    std::memcpy(out, h.data().data(), h.data().size() * sizeof(int64_t));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_fht2d_counted(const int64_t* img, int w, int h, int strategy, int64_t* hough,
+                      uint64_t* additions, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<int64_t> v;
+        if (w > 0 && h > 0) v.assign(img, img + static_cast<std::size_t>(w) * h);
+        fht::Image im = (w > 0 && h > 0) ? fht::Image(w, h, std::move(v)) : fht::Image();
+        fht::CountedTransform r = fht::fht2d_counted(im, strat(strategy));
+        copy_out(r.hough, hough);
+        if (additions) *additions = r.additions;
+    });
+}
+
+int ref_fht2d_quadrants(const int64_t* img, int w, int h, int strategy, int64_t* horiz_pos,
+                        int64_t* horiz_neg, int64_t* vert_pos, int64_t* vert_neg,
+                        uint64_t* total_additions, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        fht::Image im(w, h, std::vector<int64_t>(img, img + static_cast<std::size_t>(w) * h));
+        fht::QuadrantSet q = fht::fht2d_quadrants(im, strat(strategy), total_additions);
+        copy_out(q.horiz_pos, horiz_pos);
+        copy_out(q.horiz_neg, horiz_neg);
+        copy_out(q.vert_pos, vert_pos);
+        copy_out(q.vert_neg, vert_neg);
+    });
+}
+
+int ref_slow_hough(const int64_t* img, int w, int h, int strategy, int64_t* hough, char* err,
+                   int errlen) {
+    return guarded(err, errlen, [&] {
+        fht::Image im(w, h, std::vector<int64_t>(img, img + static_cast<std::size_t>(w) * h));
+        copy_out(fht::slow_hough(im, strat(strategy)), hough);
+    });
+}
+
+int ref_fht2d_pattern(int n, int t, int strategy, int* values, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        fht::Pattern p = fht::fht2d_pattern(n, t, strat(strategy));
+        std::memcpy(values, p.values.data(), p.values.size() * sizeof(int));
+    });
+}
+
+uint64_t ref_count_additions_tree(int w, int h, int strategy) {
+    return fht::count_additions_tree(w, h, strat(strategy));
+}
+
+// CPU baseline: n_img uint8 images (image i at img + i*w*h), all four
+// quadrants each, `threads` host threads pulling images from a shared
+// counter.  If `out` is non-null the four int64 Hough images of image i are
+// written at out + i*4*w*h (horiz_pos, horiz_neg, vert_pos, vert_neg).
+// quadrant_mask selects a subset: bit q runs quadrant q through
+// fht2d_counted on the same flipped/transposed input the reference builds.
+int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int strategy,
+                           int quadrant_mask, int threads, int64_t* out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const std::size_t cells = static_cast<std::size_t>(w) * h;
+        std::atomic<int> next{0};
+        std::atomic<int> failed{0};
+        std::string first_error;
+        auto worker = [&] {
+            for (;;) {
+                const int i = next.fetch_add(1);
+                if (i >= n_img || failed.load()) return;
+                try {
+                    std::vector<int64_t> v(cells);
+                    const uint8_t* src = img + static_cast<std::size_t>(i) * cells;
+                    for (std::size_t k = 0; k < cells; ++k) v[k] = src[k];
+                    fht::Image im(w, h, std::move(v));
+                    int64_t* dst = out ? out + static_cast<std::size_t>(i) * 4 * cells : nullptr;
+                    if (quadrant_mask == 0xF) {
+                        fht::QuadrantSet q = fht::fht2d_quadrants(im, strat(strategy));
+                        if (dst) {
+                            copy_out(q.horiz_pos, dst);
+                            copy_out(q.horiz_neg, dst + cells);
+                            copy_out(q.vert_pos, dst + 2 * cells);
+                            copy_out(q.vert_neg, dst + 3 * cells);
+                        }
+                    } else {
+                        const fht::Image tr = fht::transpose(im);
+                        const fht::Image* inputs[4] = {nullptr, nullptr, nullptr, nullptr};
+                        fht::Image flipped, flipped_tr;
+                        if (quadrant_mask & 2) flipped = fht::flip_horizontal(im);
+                        if (quadrant_mask & 8) flipped_tr = fht::flip_horizontal(tr);
+                        inputs[0] = &im;
+                        inputs[1] = &flipped;
+                        inputs[2] = &tr;
+                        inputs[3] = &flipped_tr;
+                        for (int q = 0; q < 4; ++q) {
+                            if (!(quadrant_mask & (1 << q))) continue;
+                            fht::CountedTransform r = fht::fht2d_counted(*inputs[q], strat(strategy));
+                            if (dst) copy_out(r.hough, dst + q * cells);
+                        }
+                    }
+                } catch (const std::exception& e) {
+                    if (!failed.exchange(1)) first_error = e.what();
+                    return;
+                }
+            }
+        };
+        const int nt = threads < 1 ? 1 : threads;
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nt; ++k) pool.emplace_back(worker);
+        worker();
+        for (auto& t : pool) t.join();
+        if (failed.load()) throw std::runtime_error(first_error);
+    });
+}
+
+}  // extern "C"

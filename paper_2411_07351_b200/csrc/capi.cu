@@ -1,0 +1,612 @@
+// capi.cu -- the extern "C" boundary (include/fht_b200.h) over the plan
+// tables (plan.cpp) and the sm_100a kernels (kernels.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/fht_b200.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using fhtb::GroupLaunch;
+using fhtb::QuadSet;
+using fhtb::ShapeHdr;
+using fhtb::SubPlan;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct FhtError : std::runtime_error {
+    int code;
+    FhtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw FhtError(FHT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FHT_OK;
+    } catch (const FhtError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return FHT_ERR_INVALID;
+    } catch (const std::overflow_error& e) {
+        g_last_error = e.what();
+        return FHT_ERR_OVERFLOW;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return FHT_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FHT_ERR_INTERNAL;
+    }
+}
+
+size_t esize(int dt) {
+    switch (dt) {
+        case FHT_U8: return 1;
+        case FHT_I32: return 4;
+        case FHT_I64: return 8;
+        case FHT_F32: return 4;
+    }
+    throw FhtError(FHT_ERR_INVALID, "unknown dtype");
+}
+
+bool valid_types(int in, int acc, int out) {
+    if (acc == FHT_I32 && out == FHT_I32) return in == FHT_U8 || in == FHT_I32;
+    if (acc == FHT_I32 && out == FHT_I64) return in == FHT_U8 || in == FHT_I32 || in == FHT_I64;
+    if (acc == FHT_I64 && out == FHT_I64) return in == FHT_U8 || in == FHT_I32 || in == FHT_I64;
+    if (acc == FHT_F32 && out == FHT_F32) return in == FHT_F32 || in == FHT_U8;
+    return false;
+}
+
+// Device copy of one SubPlan's tables in a single allocation.
+struct DevTables {
+    void* blob = nullptr;
+    const int4* blocks = nullptr;
+    const ShapeHdr* shapes = nullptr;
+    const int* step_offs = nullptr;
+    const int4* k1_ops = nullptr;
+    std::vector<const int4*> level_ops;
+    std::vector<int> level_nops, level_depth;
+    int max_ops = 0, max_steps = 0;
+};
+
+struct Group {
+    QuadSet qs{};
+    SubPlan sp;
+    DevTables dt;
+    int ld = 0, S = 0, sr = 0;
+    size_t slot_bytes = 0;
+};
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct fht_plan_s {
+    int w = 0, h = 0, strategy = 1, in = 0, acc = 1, out = 1, mask = 15, batch = 1, layout = 0, device = 0;
+    std::vector<std::unique_ptr<Group>> groups;
+    int chunk = 1;
+    size_t ws_bytes = 0;
+    int launches = 0;
+    uint64_t additions = 0;
+    std::mutex host_mu;
+    void* st_in = nullptr;
+    void* st_out[4] = {nullptr, nullptr, nullptr, nullptr};
+    void* st_ws = nullptr;
+
+    ~fht_plan_s() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (auto& g : groups)
+            if (g->dt.blob) cudaFree(g->dt.blob);
+        if (st_in) cudaFree(st_in);
+        for (void* p : st_out)
+            if (p) cudaFree(p);
+        if (st_ws) cudaFree(st_ws);
+        cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void upload(Group& g) {
+    const SubPlan& sp = g.sp;
+    std::vector<int4> blocks;
+    for (const auto& b : sp.blocks) blocks.push_back(make_int4(b.x0, b.shape, b.depth, 0));
+    std::vector<ShapeHdr> shapes;
+    std::vector<int> step_offs;
+    std::vector<int4> k1_ops;
+    for (const auto& s : sp.shapes) {
+        ShapeHdr hdr{};
+        hdr.width = s.width;
+        hdr.nsteps = s.depth;
+        hdr.op_base = static_cast<int>(k1_ops.size());
+        hdr.step_base = static_cast<int>(step_offs.size());
+        hdr.halo = s.halo;
+        shapes.push_back(hdr);
+        for (int o : s.step_offset) step_offs.push_back(o);
+        for (size_t k = 0; k < s.ops.size(); ++k) {
+            const auto& op = s.ops[k];
+            if (op.r < 0 || op.r > 0xffff || s.extra[k] > 0x7fff) throw FhtError(FHT_ERR_INTERNAL, "k1 op overflow");
+            k1_ops.push_back(make_int4(op.dst, op.a, op.b, op.r | (s.extra[k] << 16)));
+        }
+        g.dt.max_ops = std::max(g.dt.max_ops, static_cast<int>(s.ops.size()));
+        g.dt.max_steps = std::max(g.dt.max_steps, s.depth);
+    }
+    // Assemble one blob, 16-byte aligned sections.
+    std::vector<char> blob;
+    auto put = [&](const void* p, size_t n) {
+        size_t off = (blob.size() + 15) / 16 * 16;
+        blob.resize(off + n);
+        if (n) std::memcpy(blob.data() + off, p, n);
+        return off;
+    };
+    const size_t o_blocks = put(blocks.data(), blocks.size() * sizeof(int4));
+    const size_t o_shapes = put(shapes.data(), shapes.size() * sizeof(ShapeHdr));
+    const size_t o_steps = put(step_offs.data(), step_offs.size() * sizeof(int));
+    const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(int4));
+    std::vector<size_t> o_levels;
+    for (const auto& lvl : sp.levels) {
+        std::vector<int4> ops;
+        for (const auto& op : lvl.ops) ops.push_back(make_int4(op.dst, op.a, op.b, op.r));
+        o_levels.push_back(put(ops.data(), ops.size() * sizeof(int4)));
+        g.dt.level_nops.push_back(static_cast<int>(ops.size()));
+        g.dt.level_depth.push_back(lvl.depth);
+    }
+    blob.resize(blob.size() + 16);
+    cuda_check(cudaMalloc(&g.dt.blob, blob.size()), "cudaMalloc(plan tables)");
+    cuda_check(cudaMemcpy(g.dt.blob, blob.data(), blob.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan tables)");
+    char* base = static_cast<char*>(g.dt.blob);
+    g.dt.blocks = reinterpret_cast<const int4*>(base + o_blocks);
+    g.dt.shapes = reinterpret_cast<const ShapeHdr*>(base + o_shapes);
+    g.dt.step_offs = reinterpret_cast<const int*>(base + o_steps);
+    g.dt.k1_ops = reinterpret_cast<const int4*>(base + o_k1);
+    for (size_t o : o_levels) g.dt.level_ops.push_back(reinterpret_cast<const int4*>(base + o));
+}
+
+int block_width_default() {
+    if (const char* e = std::getenv("FHT_BLOCK_WIDTH")) return std::max(1, std::min(64, std::atoi(e)));
+    return 32;
+}
+
+fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, int mask, int batch, int layout,
+                        int device) {
+    if (w < 1 || h < 1) throw std::invalid_argument("fht2d: image is empty");
+    if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED)
+        throw std::invalid_argument("unknown strategy (expected simple|tweaked)");
+    if (!valid_types(in, acc, out)) throw std::invalid_argument("unsupported (input, accumulator, output) dtype triple");
+    if (mask < 1 || mask > 15) throw std::invalid_argument("quadrant mask must select 1..4 quadrants");
+    if (batch < 1) throw std::invalid_argument("batch must be >= 1");
+    if (layout != FHT_LAYOUT_REFERENCE && layout != FHT_LAYOUT_NATIVE) throw std::invalid_argument("unknown layout");
+    if (static_cast<int64_t>(w) * h > (int64_t(1) << 31) - 1) throw std::invalid_argument("image too large");
+    // Static overflow budget for u8 into int32 (transform.cpp:16-27 with vmax = 255).
+    const bool uses_h = (mask & (FHT_VERT_POS | FHT_VERT_NEG)) != 0, uses_w = (mask & 3) != 0;
+    const int64_t wmax = std::max<int64_t>(uses_w ? w : 0, uses_h ? h : 0);
+    if (in == FHT_U8 && acc == FHT_I32 && wmax * 255 >= (int64_t(1) << 31))
+        throw std::overflow_error("fht2d: width * 255 reaches 2^31; use an int64 accumulator");
+    int ndev = 0;
+    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("no such CUDA device");
+    DeviceGuard dg(device);
+
+    auto p = std::make_unique<fht_plan_s>();
+    p->w = w, p->h = h, p->strategy = strategy, p->in = in, p->acc = acc, p->out = out, p->mask = mask;
+    p->batch = batch, p->layout = layout, p->device = device;
+    const int bw = block_width_default();
+    const size_t acc_sz = esize(acc);
+
+    // Orientation groups: horizontal quadrants work on (W=w, H=h), vertical on
+    // (W=h, H=w).  A square image shares one table set across all four.
+    std::vector<std::pair<int, std::vector<int>>> orient;  // (horizontal?, codes)
+    std::vector<int> hq, vq;
+    for (int q = 0; q < 4; ++q)
+        if (mask & (1 << q)) (q < 2 ? hq : vq).push_back(q);
+    if (w == h) {
+        std::vector<int> all = hq;
+        all.insert(all.end(), vq.begin(), vq.end());
+        orient.push_back({1, all});
+    } else {
+        if (!hq.empty()) orient.push_back({1, hq});
+        if (!vq.empty()) orient.push_back({0, vq});
+    }
+    size_t max_slot_bytes = 0;
+    int max_nq = 0;
+    for (auto& [horizontal, codes] : orient) {
+        auto g = std::make_unique<Group>();
+        const int W = horizontal ? w : h, H = horizontal ? h : w;
+        g->sp = SubPlan::build(W, H, strategy, bw);
+        g->qs.n = static_cast<int>(codes.size());
+        for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
+        g->ld = round_up(H, acc_sz == 8 ? 16 : 32);
+        int S = acc_sz == 8 ? 128 : 256;
+        if (H < S) S = H;
+        g->S = S;
+        g->sr = S + g->sp.max_halo;
+        if ((g->sr & 1) == 0) g->sr += 1;
+        g->slot_bytes = g->sp.root_is_block ? 0 : 2 * static_cast<size_t>(W) * g->ld * acc_sz;
+        upload(*g);
+        const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
+        if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
+        max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
+        max_nq = std::max(max_nq, g->qs.n);
+        p->additions += g->sp.additions * static_cast<uint64_t>(g->qs.n) * static_cast<uint64_t>(batch);
+        p->groups.push_back(std::move(g));
+    }
+    // Images per chunk: all of them unless FHT_CHUNK_IMAGES asks otherwise or
+    // grid.z (65535 slots) / the 16 GiB workspace cap forces a split.
+    int chunk = batch;
+    if (const char* e = std::getenv("FHT_CHUNK_IMAGES")) chunk = std::max(1, std::min(batch, std::atoi(e)));
+    chunk = std::min(chunk, 65535 / std::max(1, max_nq));
+    const size_t cap = size_t(16) << 30;
+    if (max_slot_bytes > 0) chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(chunk, cap / max_slot_bytes)));
+    p->chunk = chunk;
+    p->ws_bytes = max_slot_bytes * static_cast<size_t>(chunk);
+    const int nchunks = (batch + chunk - 1) / chunk;
+    int per_chunk = 0;
+    for (auto& g : p->groups) per_chunk += 1 + (g->sp.root_is_block ? 0 : static_cast<int>(g->sp.levels.size()));
+    p->launches = per_chunk * nchunks;
+    return p.release();
+}
+
+void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_out[4], int64_t out_stride,
+             void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr) {
+    if (!d_in) throw std::invalid_argument("fht_execute: null input");
+    for (int q = 0; q < 4; ++q)
+        if ((p->mask & (1 << q)) && !d_out[q]) throw std::invalid_argument("fht_execute: null output for a selected quadrant");
+    if (p->ws_bytes && !ws) throw std::invalid_argument("fht_execute: null workspace");
+    DeviceGuard dg(p->device);
+    for (int img0 = 0; img0 < p->batch; img0 += p->chunk) {
+        const int nimg = std::min(p->chunk, p->batch - img0);
+        for (auto& gp : p->groups) {
+            Group& g = *gp;
+            GroupLaunch L{};
+            L.img = d_in;
+            L.in_dtype = p->in;
+            L.img_w = p->w;
+            L.img_h = p->h;
+            L.img_stride = in_stride;
+            L.img0 = img0;
+            L.nimg = nimg;
+            L.qs = g.qs;
+            L.W = g.sp.W;
+            L.H = g.sp.H;
+            L.ld = g.ld;
+            L.acc_dtype = p->acc;
+            L.S = g.S;
+            L.nblocks = static_cast<int>(g.sp.blocks.size());
+            L.blocks = g.dt.blocks;
+            L.shapes = g.dt.shapes;
+            L.step_offs = g.dt.step_offs;
+            L.k1_ops = g.dt.k1_ops;
+            L.k1_max_ops = g.dt.max_ops;
+            L.k1_max_steps = g.dt.max_steps;
+            L.k1_max_width = g.sp.max_block_width;
+            L.k1_sr = g.sr;
+            L.root_is_block = g.sp.root_is_block;
+            L.nlevels = static_cast<int>(g.dt.level_ops.size());
+            L.level_ops = g.dt.level_ops.data();
+            L.level_nops = g.dt.level_nops.data();
+            L.level_depth = g.dt.level_depth.data();
+            L.ws = ws;
+            for (int q = 0; q < 4; ++q) L.out.ptr[q] = d_out[q];
+            L.out.img_stride = out_stride;
+            L.out.layout = p->layout;
+            L.out.dtype = p->out;
+            if (fhtb::launch_group(L, st, hook, ctx) < 0) throw FhtError(FHT_ERR_INVALID, "unsupported dtype triple");
+            cuda_check(cudaGetLastError(), "kernel launch");
+        }
+    }
+}
+
+size_t cells_of(const fht_plan_s* p) { return static_cast<size_t>(p->w) * p->h; }
+
+void execute_host(fht_plan_s* p, const void* h_in, void* const h_out[4], cudaStream_t st) {
+    if (!h_in) throw std::invalid_argument("fht_execute_host: null input");
+    std::lock_guard<std::mutex> lk(p->host_mu);
+    DeviceGuard dg(p->device);
+    const size_t cells = cells_of(p);
+    const size_t in_bytes = cells * esize(p->in) * p->batch, out_bytes = cells * esize(p->out) * p->batch;
+    if (!p->st_in) cuda_check(cudaMalloc(&p->st_in, in_bytes), "cudaMalloc(staging in)");
+    for (int q = 0; q < 4; ++q)
+        if ((p->mask & (1 << q)) && !p->st_out[q]) cuda_check(cudaMalloc(&p->st_out[q], out_bytes), "cudaMalloc(staging out)");
+    if (p->ws_bytes && !p->st_ws) cuda_check(cudaMalloc(&p->st_ws, p->ws_bytes), "cudaMalloc(workspace)");
+    cuda_check(cudaMemcpyAsync(p->st_in, h_in, in_bytes, cudaMemcpyHostToDevice, st), "H2D");
+    execute(p, p->st_in, static_cast<int64_t>(cells), p->st_out, static_cast<int64_t>(cells), p->st_ws, st);
+    for (int q = 0; q < 4; ++q)
+        if (p->mask & (1 << q)) {
+            if (!h_out[q]) throw std::invalid_argument("fht_execute_host: null output for a selected quadrant");
+            cuda_check(cudaMemcpyAsync(h_out[q], p->st_out[q], out_bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+}
+
+// absmax on device -> (ok_for_i32, within 2^62 budget)
+void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok_i32, cudaStream_t st) {
+    if (dtype == FHT_U8) {
+        if (ok_i32) *ok_i32 = static_cast<int64_t>(width) * 255 < (int64_t(1) << 31);
+        return;
+    }
+    if (dtype == FHT_F32) throw std::invalid_argument("check_budget: integer inputs only");
+    unsigned long long* d_max = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_max), sizeof(unsigned long long), st), "cudaMallocAsync");
+    cuda_check(cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
+    fhtb::launch_absmax(d_in, dtype, count, d_max, st);
+    unsigned long long vmax = 0;
+    cuda_check(cudaMemcpyAsync(&vmax, d_max, sizeof(vmax), cudaMemcpyDeviceToHost, st), "D2H(absmax)");
+    cuda_check(cudaFreeAsync(d_max, st), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    const unsigned __int128 prod = static_cast<unsigned __int128>(static_cast<unsigned>(width)) * vmax;
+    if (prod >= (static_cast<unsigned __int128>(1) << 62))
+        throw std::overflow_error("fht2d: width * max|value| reaches 2^62; sums could overflow 64-bit accumulators");
+    if (ok_i32) *ok_i32 = prod < (static_cast<unsigned __int128>(1) << 31);
+}
+
+// Per-device cache of plans used by the int64 reference entry points.
+std::mutex g_cache_mu;
+std::map<std::tuple<int, int, int, int, int, int>, std::unique_ptr<fht_plan_s>> g_cache;
+
+fht_plan_s* cached_plan(int w, int h, int strategy, int acc, int mask, int device) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto key = std::make_tuple(w, h, strategy, acc, mask, device);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second.get();
+    fht_plan_s* p = create_plan(w, h, strategy, FHT_I64, acc, FHT_I64, mask, 1, FHT_LAYOUT_REFERENCE, device);
+    g_cache.emplace(key, std::unique_ptr<fht_plan_s>(p));
+    return p;
+}
+
+void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* const outs[4], uint64_t* adds) {
+    if (w < 1 || h < 1 || !img) throw std::invalid_argument("fht2d: image is empty");
+    if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED)
+        throw std::invalid_argument("unknown strategy (expected simple|tweaked)");
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t cells = static_cast<size_t>(w) * h;
+    void* d_in = nullptr;
+    void* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
+    void* d_ws = nullptr;
+    auto release = [&] {
+        if (d_in) cudaFreeAsync(d_in, st);
+        for (void* q : d_out)
+            if (q) cudaFreeAsync(q, st);
+        if (d_ws) cudaFreeAsync(d_ws, st);
+        cudaStreamSynchronize(st);
+    };
+    try {
+        cuda_check(cudaMallocAsync(&d_in, cells * 8, st), "cudaMallocAsync(in)");
+        cuda_check(cudaMemcpyAsync(d_in, img, cells * 8, cudaMemcpyHostToDevice, st), "H2D");
+        // check_overflow_budget (transform.cpp:16-27) for every quadrant's working width.
+        int ok32 = 0;
+        const int wmax = std::max((mask & 3) ? w : 0, (mask & 12) ? h : 0);
+        check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), wmax, &ok32, st);
+        fht_plan_s* p = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev);
+        for (int q = 0; q < 4; ++q)
+            if (mask & (1 << q)) cuda_check(cudaMallocAsync(&d_out[q], cells * 8, st), "cudaMallocAsync(out)");
+        if (p->ws_bytes) cuda_check(cudaMallocAsync(&d_ws, p->ws_bytes, st), "cudaMallocAsync(ws)");
+        execute(p, d_in, static_cast<int64_t>(cells), d_out, static_cast<int64_t>(cells), d_ws, st);
+        for (int q = 0; q < 4; ++q)
+            if (mask & (1 << q)) cuda_check(cudaMemcpyAsync(outs[q], d_out[q], cells * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        if (adds) *adds = p->additions;
+    } catch (...) {
+        release();
+        throw;
+    }
+    release();
+}
+
+}  // namespace
+
+extern "C" {
+
+int fht_plan_create(int width, int height, int strategy, int in_dtype, int acc_dtype, int out_dtype,
+                    int quadrant_mask, int batch, int layout, int device, fht_plan_t* plan) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan pointer");
+        *plan = create_plan(width, height, strategy, in_dtype, acc_dtype, out_dtype, quadrant_mask, batch, layout,
+                            device);
+    });
+}
+
+int fht_plan_destroy(fht_plan_t plan) {
+    return guarded([&] { delete plan; });
+}
+
+size_t fht_workspace_bytes(fht_plan_t plan) { return plan ? plan->ws_bytes : 0; }
+
+uint64_t fht_additions(fht_plan_t plan) { return plan ? plan->additions : 0; }
+
+int fht_launches_per_execute(fht_plan_t plan) { return plan ? plan->launches : 0; }
+
+int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
+    return guarded([&] {
+        if (!plan || !buf || !len) throw std::invalid_argument("fht_plan_describe: null argument");
+        std::ostringstream o;
+        o << "{\"width\":" << plan->w << ",\"height\":" << plan->h << ",\"batch\":" << plan->batch
+          << ",\"chunk\":" << plan->chunk << ",\"workspace_bytes\":" << plan->ws_bytes
+          << ",\"launches\":" << plan->launches << ",\"additions\":" << plan->additions << ",\"groups\":[";
+        for (size_t i = 0; i < plan->groups.size(); ++i) {
+            const Group& g = *plan->groups[i];
+            o << (i ? "," : "") << "{\"quadrants\":[";
+            for (int k = 0; k < g.qs.n; ++k) o << (k ? "," : "") << g.qs.code[k];
+            o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"plan\":" << g.sp.describe() << "}";
+        }
+        o << "]}";
+        const std::string s = o.str();
+        if (s.size() + 1 > len) throw std::invalid_argument("fht_plan_describe: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
+                int64_t out_image_stride, void* d_workspace, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_out) throw std::invalid_argument("fht_execute: null argument");
+        execute(plan, d_in, in_image_stride, d_out, out_image_stride, d_workspace, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
+                         int64_t out_image_stride, void* d_workspace, void* stream, float* launch_ms, int* launch_kind,
+                         int max_launches, int* n_launches) {
+    struct Ctx {
+        cudaStream_t st;
+        std::vector<cudaEvent_t> ev;
+        std::vector<int> kind;
+    };
+    Ctx c;
+    c.st = static_cast<cudaStream_t>(stream);
+    auto hook = [](void* vp, int kind) {
+        Ctx* cx = static_cast<Ctx*>(vp);
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, cx->st);
+        cx->ev.push_back(e);
+        cx->kind.push_back(kind);
+    };
+    const int rc = guarded([&] {
+        if (!plan || !d_out) throw std::invalid_argument("fht_execute_profiled: null argument");
+        DeviceGuard dg(plan->device);
+        cudaEvent_t e0;
+        cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
+        cuda_check(cudaEventRecord(e0, c.st), "cudaEventRecord");
+        c.ev.push_back(e0);
+        c.kind.push_back(0);
+        execute(plan, d_in, in_image_stride, d_out, out_image_stride, d_workspace, c.st, hook, &c);
+        cuda_check(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+        const int n = static_cast<int>(c.ev.size()) - 1;
+        if (n_launches) *n_launches = n;
+        for (int i = 0; i < n && i < max_launches; ++i) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, c.ev[static_cast<size_t>(i)], c.ev[static_cast<size_t>(i) + 1]),
+                       "cudaEventElapsedTime");
+            if (launch_ms) launch_ms[i] = ms;
+            if (launch_kind) launch_kind[i] = c.kind[static_cast<size_t>(i) + 1];
+        }
+    });
+    for (cudaEvent_t e : c.ev) cudaEventDestroy(e);
+    return rc;
+}
+
+int fht_execute_host(fht_plan_t plan, const void* h_in, void* const h_out[4], void* stream) {
+    return guarded([&] {
+        if (!plan || !h_out) throw std::invalid_argument("fht_execute_host: null argument");
+        execute_host(plan, h_in, h_out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fht_check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok_for_i32, void* stream) {
+    return guarded([&] { check_budget(d_in, dtype, count, width, ok_for_i32, static_cast<cudaStream_t>(stream)); });
+}
+
+int fht_fht2d_counted_i64(const int64_t* img, int width, int height, int strategy, int64_t* hough,
+                          uint64_t* additions) {
+    return guarded([&] {
+        int64_t* outs[4] = {hough, nullptr, nullptr, nullptr};
+        run_i64(img, width, height, strategy, FHT_HORIZ_POS, outs, additions);
+    });
+}
+
+int fht_fht2d_quadrants_i64(const int64_t* img, int width, int height, int strategy, int64_t* horiz_pos,
+                            int64_t* horiz_neg, int64_t* vert_pos, int64_t* vert_neg, uint64_t* total_additions) {
+    return guarded([&] {
+        int64_t* outs[4] = {horiz_pos, horiz_neg, vert_pos, vert_neg};
+        run_i64(img, width, height, strategy, FHT_ALL_QUADRANTS, outs, total_additions);
+    });
+}
+
+int fht_split_width(int w, int strategy, int* w0, int* w1) {
+    return guarded([&] {
+        if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED) throw std::invalid_argument("unknown strategy");
+        auto pr = fhtb::split_width(w, strategy);
+        if (w0) *w0 = pr.first;
+        if (w1) *w1 = pr.second;
+    });
+}
+
+int fht_round_half_up_ratio(int64_t num, int64_t den, int64_t* result) {
+    return guarded([&] {
+        const int64_t v = fhtb::round_half_up_ratio(num, den);
+        if (result) *result = v;
+    });
+}
+
+int fht_count_additions_tree(int w, int h, int strategy, uint64_t* result) {
+    return guarded([&] {
+        const uint64_t v = fhtb::count_additions_tree(w, h, strategy);
+        if (result) *result = v;
+    });
+}
+
+int fht_schedule_json(int W, int H, int strategy, int block_width, char* buf, size_t len, size_t* needed) {
+    return guarded([&] {
+        const SubPlan sp = SubPlan::build(W, H, strategy, block_width);
+        std::ostringstream o;
+        o << "{\"W\":" << sp.W << ",\"H\":" << sp.H << ",\"root_is_block\":" << (sp.root_is_block ? 1 : 0)
+          << ",\"additions\":" << sp.additions << ",\"blocks\":[";
+        for (size_t i = 0; i < sp.blocks.size(); ++i)
+            o << (i ? "," : "") << "[" << sp.blocks[i].x0 << "," << sp.blocks[i].shape << "," << sp.blocks[i].depth << "]";
+        o << "],\"shapes\":[";
+        for (size_t i = 0; i < sp.shapes.size(); ++i) {
+            const auto& s = sp.shapes[i];
+            o << (i ? "," : "") << "{\"width\":" << s.width << ",\"steps\":" << s.depth << ",\"halo\":" << s.halo
+              << ",\"step_offset\":[";
+            for (size_t k = 0; k < s.step_offset.size(); ++k) o << (k ? "," : "") << s.step_offset[k];
+            o << "],\"ops\":[";
+            for (size_t k = 0; k < s.ops.size(); ++k)
+                o << (k ? "," : "") << "[" << s.ops[k].dst << "," << s.ops[k].a << "," << s.ops[k].b << "," << s.ops[k].r
+                  << "," << s.extra[k] << "]";
+            o << "]}";
+        }
+        o << "],\"levels\":[";
+        for (size_t i = 0; i < sp.levels.size(); ++i) {
+            o << (i ? "," : "") << "{\"depth\":" << sp.levels[i].depth << ",\"ops\":[";
+            for (size_t k = 0; k < sp.levels[i].ops.size(); ++k) {
+                const auto& op = sp.levels[i].ops[k];
+                o << (k ? "," : "") << "[" << op.dst << "," << op.a << "," << op.b << "," << op.r << "]";
+            }
+            o << "]}";
+        }
+        o << "]}";
+        const std::string s = o.str();
+        if (needed) *needed = s.size() + 1;
+        if (!buf || s.size() + 1 > len) throw std::invalid_argument("fht_schedule_json: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+const char* fht_last_error(void) { return g_last_error.c_str(); }
+
+const char* fht_version(void) { return "fht_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// kernels.cuh -- launch interface of the sm_100a FHT2D merge kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fhtb {
+
+enum DType : int { kU8 = 0, kI32 = 1, kI64 = 2, kF32 = 3 };
+
+// Quadrant codes (reference QuadrantSet order, quadrants.hpp:23-28):
+//   0 horiz_pos = fht2d(I)            COLS[x][y] = I[y][x]
+//   1 horiz_neg = fht2d(flipH(I))     COLS[x][y] = I[y][w-1-x]
+//   2 vert_pos  = fht2d(I^T)          COLS[x][y] = I[x][y]
+//   3 vert_neg  = fht2d(flipH(I^T))   COLS[x][y] = I[h-1-x][y]
+struct QuadSet {
+    int code[4];
+    int n;
+};
+
+// Output of the root level.  ptr[q] is the quadrant-q Hough image of image
+// 0; image i is at ptr[q] + i * img_stride elements.  layout 0 is the
+// reference layout hough[s * W + t] (transform.cpp:80-83); layout 1 is the
+// native slope-major layout hough[t * H + s].
+struct OutDesc {
+    void* ptr[4];
+    long long img_stride;
+    int layout;
+    int dtype;
+};
+
+// Per K1 shape header (8 ints): width, nsteps, op_base, step_base, halo.
+struct ShapeHdr {
+    int width, nsteps, op_base, step_base, halo, pad0, pad1, pad2;
+};
+
+struct GroupLaunch {
+    // image
+    const void* img;
+    int in_dtype;
+    int img_w, img_h;
+    long long img_stride;
+    int img0;      // first image of this chunk
+    int nimg;      // images in this chunk
+    QuadSet qs;
+    // working orientation
+    int W, H, ld;
+    int acc_dtype;
+    // K1
+    int S;
+    int nblocks;
+    const int4* blocks;
+    const ShapeHdr* shapes;
+    const int* step_offs;
+    const int4* k1_ops;
+    int k1_max_ops, k1_max_steps, k1_max_width, k1_sr;
+    bool root_is_block;
+    // upper levels, deepest first; the last is the root when !root_is_block
+    int nlevels;
+    const int4* const* level_ops;
+    const int* level_nops;
+    const int* level_depth;
+    // workspace: per slot two W x ld buffers
+    void* ws;
+    OutDesc out;
+};
+
+size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps);
+// Launch every kernel of one orientation group / chunk on `stream`.
+// Returns the number of kernel launches, or -1 on an unsupported type combination.
+// `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1, 2 = K2, 3 = K3.
+typedef void (*LaunchHook)(void* ctx, int kind);
+int launch_group(const GroupLaunch& g, cudaStream_t stream, LaunchHook hook = nullptr, void* ctx = nullptr);
+
+// Device max |v| over n int32/int64 values into *d_max (must be zeroed).
+void launch_absmax(const void* d_in, int dtype, long long n, unsigned long long* d_max, cudaStream_t stream);
+
+}  // namespace fhtb

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle.
+
+Bar: bit-exact for integer inputs; for float32, bit-exact against the fp32
+restatement of the same add tree AND max |J - J64| <= 1e-5 * L1 (L1 = the
+fp64 transform of |I|), the tolerance BASELINE.json states.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_07351_b200 import fht, workloads
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+Q = oracle.QUADRANTS
+
+
+def run_plan(imgs, in_dtype, acc, strategy=1, quadrants="all", layout="reference", out_dtype=None):
+    imgs = np.ascontiguousarray(imgs)
+    if imgs.ndim == 2:
+        imgs = imgs[None]
+    b, h, w = imgs.shape
+    plan = fht.Plan(w, h, strategy, in_dtype=in_dtype, acc_dtype=acc, out_dtype=out_dtype, quadrants=quadrants,
+                    batch=b, layout=layout)
+    x = torch.from_numpy(imgs).cuda()
+    out = plan(x)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}, plan
+
+
+# ------------------------------------------------- reference entry points
+def test_golden_vectors_through_c_abi(golden):
+    for row in golden["meta"]:
+        i, h, w, strat, adds, qadds = (int(v) for v in row)
+        img = golden[f"c{i}_img"].astype(np.int64)
+        ct = fht.fht2d_counted(img, strat)
+        np.testing.assert_array_equal(ct.hough, golden[f"c{i}_s{strat}_fht2d"])
+        assert ct.additions == adds
+        tot = []
+        qs = fht.fht2d_quadrants(img, strat, tot)
+        assert tot == [qadds]
+        for k in Q:
+            np.testing.assert_array_equal(getattr(qs, k), golden[f"c{i}_s{strat}_{k}"])
+
+
+def test_spec_2x2_and_identity():
+    a, b, c, d = 3, 5, 7, 11
+    j = fht.fht2d(np.array([[a, b], [c, d]]), "tweaked")
+    assert j[0, 0] == a + b and j[1, 0] == c + d and j[0, 1] == a + d and j[1, 1] == c + b
+    col = np.arange(9).reshape(9, 1)
+    np.testing.assert_array_equal(fht.fht2d(col), col)  # w = 1 -> identity
+    assert fht.fht2d_counted(col).additions == 0
+
+
+def test_int64_values_use_int64_accumulation():
+    rng = np.random.default_rng(11)
+    img = rng.integers(-(1 << 40), 1 << 40, (37, 53))
+    for s in (0, 1):
+        np.testing.assert_array_equal(fht.fht2d(img, s), oracle.fht2d_counted_i64(img, s)[0])
+
+
+def test_errors_mirror_reference():
+    with pytest.raises(fht.OverflowBudget):
+        fht.fht2d(np.full((3, 4), 1 << 61, dtype=np.int64))
+    with pytest.raises(fht.InvalidArgument):
+        fht.fht2d(np.zeros((0, 4), dtype=np.int64))
+    with pytest.raises(fht.InvalidArgument):
+        fht.fht2d(np.zeros((2, 2), dtype=np.int64), 7)
+    with pytest.raises(fht.InvalidArgument):
+        fht.Plan(0, 5)
+    with pytest.raises(fht.OverflowBudget):
+        fht.Plan(9_000_000, 1, in_dtype="u8", acc_dtype="i32", quadrants="horiz_pos")
+
+
+# ---------------------------------------------------------- plan API
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_small_sizes_all_quadrants_batched(strategy):
+    rng = np.random.default_rng(100 + strategy)
+    for (h, w) in [(1, 1), (1, 9), (9, 1), (2, 2), (3, 5), (17, 17), (31, 33), (33, 31), (40, 64), (64, 40),
+                   (65, 65), (100, 7), (7, 100), (129, 130)]:
+        imgs = rng.integers(0, 256, (3, h, w), dtype=np.uint8)
+        out, plan = run_plan(imgs, "u8", "i32", strategy)
+        for bi in range(3):
+            ref, adds = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+            for k in Q:
+                np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} {k} img{bi}")
+        assert plan.additions == 3 * adds
+
+
+def test_native_layout_and_widening():
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (45, 77), dtype=np.uint8)
+    ref, _ = oracle.fht2d_quadrants(img, 1)
+    out, _ = run_plan(img, "u8", "i32", layout="native")
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k].T)
+    out, _ = run_plan(img, "u8", "i32", out_dtype="i64")
+    for k in Q:
+        assert out[k].dtype == np.int64
+        np.testing.assert_array_equal(out[k][0], ref[k])
+    out, _ = run_plan(img, "u8", "i64")
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
+
+
+def test_int32_inputs_with_negative_values():
+    rng = np.random.default_rng(6)
+    img = rng.integers(-(1 << 20), 1 << 20, (70, 90)).astype(np.int32)
+    out, _ = run_plan(img, "i32", "i32", strategy=0)
+    ref, _ = oracle.fht2d_quadrants(img, 0, dtype=np.int32)
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
+
+
+def test_float32_small_bit_exact_vs_fp32_tree():
+    rng = np.random.default_rng(8)
+    for (h, w) in [(37, 53), (64, 64), (200, 131)]:
+        img = rng.standard_normal((h, w)).astype(np.float32)
+        out, _ = run_plan(img, "f32", "f32")
+        ref, _ = oracle.fht2d_quadrants(img, 1, dtype=np.float32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][0], ref[k])
+
+
+# --------------------------------------------------- the five configs
+def _cfg_plan(cfg, count=None):
+    c = workloads.CONFIGS[cfg]
+    imgs = workloads.make_images(cfg, count)
+    out, plan = run_plan(imgs, c.dtype, c.acc, 1, quadrants=list(c.quadrants))
+    return c, imgs, out, plan
+
+
+def test_config_c1_bit_exact():
+    c, imgs, out, plan = _cfg_plan("c1")
+    ref, adds = oracle.fht2d(imgs[0].T, 1, dtype=np.int32)  # vert_pos = fht2d(I^T)
+    np.testing.assert_array_equal(out["vert_pos"][0], ref)
+    assert plan.additions == adds == 9_984_000
+    # the reference's own fht2d(I) family (horiz_pos) as a parity extra
+    out2, _ = run_plan(imgs, "u8", "i32", 1, quadrants="horiz_pos")
+    np.testing.assert_array_equal(out2["horiz_pos"][0], oracle.fht2d(imgs[0], 1, dtype=np.int32)[0])
+
+
+def test_config_c2_bit_exact_and_strategies_coincide():
+    c, imgs, out, plan = _cfg_plan("c2")
+    ref, adds = oracle.fht2d_quadrants(imgs[0], 1, dtype=np.int32)
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
+    assert plan.additions == adds == 4 * 10_485_760
+    out_s, _ = run_plan(imgs, "u8", "i32", 0)
+    for k in Q:
+        np.testing.assert_array_equal(out_s[k], out[k])  # Simple == Tweaked at n = 2^q
+
+
+def _float_check(img, out, quadrant):
+    """bit-exact vs the fp32 tree and within 1e-5 * L1 of the fp64 tree."""
+    src = {"horiz_pos": img, "horiz_neg": img[:, ::-1], "vert_pos": img.T, "vert_neg": img.T[:, ::-1]}[quadrant]
+    src = np.ascontiguousarray(src)
+    j32, _ = oracle.fht2d(src, 1, dtype=np.float32)
+    np.testing.assert_array_equal(out, j32)
+    j64, _ = oracle.fht2d(src.astype(np.float64), 1, dtype=np.float64)
+    l1, _ = oracle.fht2d(np.abs(src).astype(np.float64), 1, dtype=np.float64)
+    err = np.abs(out.astype(np.float64) - j64) / l1
+    assert err.max() <= 1e-5, err.max()
+
+
+def test_config_c3_float32():
+    c, imgs, out, plan = _cfg_plan("c3")
+    for k in Q:
+        _float_check(imgs[0], out[k][0], k)
+
+
+def test_config_c4_batch():
+    c, imgs, out, plan = _cfg_plan("c4")
+    assert out["horiz_pos"].shape == (256, 509, 509)
+    rng = np.random.default_rng(0)
+    for bi in sorted(rng.choice(256, 24, replace=False)):  # full oracle compare on a seeded sample
+        ref, _ = oracle.fht2d_quadrants(imgs[bi], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][bi], ref[k])
+    # every image: mass conservation per slope, a size-independent property
+    mass = imgs.reshape(256, -1).sum(axis=1).astype(np.int64)
+    for k in Q:
+        col = out[k].astype(np.int64).sum(axis=1)  # sum over s -> (256, W)
+        assert (col == mass[:, None]).all()
+
+
+def test_config_c5_float32():
+    c, imgs, out, plan = _cfg_plan("c5")
+    img = imgs[0]
+    for k in ("horiz_pos", "vert_neg"):  # two quadrants against the full oracle (~10 s each)
+        _float_check(img, out[k][0], k)
+    tot = float(img.astype(np.float64).sum())
+    for k in Q:  # all four: mass conservation within fp32 rounding
+        col = out[k][0].astype(np.float64).sum(axis=0)
+        assert np.allclose(col, tot, rtol=1e-4)
+
+
+def test_shift_equivariance_and_linearity_large():
+    rng = np.random.default_rng(9)
+    n = 1000
+    a = rng.integers(0, 100, (n, n), dtype=np.int32)
+    b = rng.integers(0, 100, (n, n), dtype=np.int32)
+    ja, _ = run_plan(a, "i32", "i32")
+    jb, _ = run_plan(b, "i32", "i32")
+    jab, _ = run_plan(3 * a + 2 * b, "i32", "i32")
+    for k in Q:
+        np.testing.assert_array_equal(jab[k], 3 * ja[k] + 2 * jb[k])
+    r = 37
+    jr, _ = run_plan(np.roll(a, -r, axis=0), "i32", "i32", quadrants="horiz_pos")
+    np.testing.assert_array_equal(jr["horiz_pos"][0], np.roll(ja["horiz_pos"][0], -r, axis=0))
+
+
+def test_execute_host_roundtrip():
+    rng = np.random.default_rng(12)
+    imgs = rng.integers(0, 256, (4, 61, 67), dtype=np.uint8)
+    plan = fht.Plan(67, 61, 1, in_dtype="u8", acc_dtype="i32", batch=4)
+    out = plan.execute_host(imgs)
+    for bi in range(4):
+        ref, _ = oracle.fht2d_quadrants(imgs[bi], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][bi], ref[k])
