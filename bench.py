@@ -197,13 +197,14 @@ def run_reference(args):
 ESZ = {"u8": 1, "i32": 4, "i64": 8, "f32": 4}
 
 
-def algorithmic_bytes(plan: fht.Plan, c: workloads.Config, kind: int, nops: int, W: int, H: int, slots: int):
-    """each distinct input cell read once, each output cell
-    written once, per launch.  K1: W*H*(e_in + e_acc); K2/K3: nops*H*2*e_acc."""
+def algorithmic_bytes(c: workloads.Config, kind: int, W: int, H: int, slots: int):
+    """per launch, each distinct input cell read once and each
+    output cell written once.  K1 (image -> pass-0 frontier): W*H*(e_in + e_acc);
+    a fused K2 pass (frontier -> next frontier / root): W*H*2*e_acc."""
     ea = ESZ[c.acc]
     if kind == 1:
         return slots * W * H * (ESZ[c.dtype] + ea)
-    return slots * nops * H * 2 * ea
+    return slots * W * H * 2 * ea
 
 
 def run_ours(args):
@@ -284,22 +285,17 @@ def run_ours(args):
     # Map each launch to its byte count.
     g = desc["groups"][0]
     sp = g["plan"]
-    slots_total = c.batch * len(g["quadrants"])
-    chunk_slots = desc["chunk"] * len(g["quadrants"])
     launch_bytes = []
-    lvl_nops = [lv["ops"] for lv in sp["levels"]]
-    k = 0
     for img0 in range(0, c.batch, desc["chunk"]):
         nimg = min(desc["chunk"], c.batch - img0)
         slots = nimg * len(g["quadrants"])
-        launch_bytes.append(algorithmic_bytes(plan, c, 1, 0, sp["W"], sp["H"], slots))
-        if not sp["root_is_block"]:
-            for nops in lvl_nops:
-                launch_bytes.append(algorithmic_bytes(plan, c, 2, nops, sp["W"], sp["H"], slots))
+        launch_bytes.append(algorithmic_bytes(c, 1, sp["W"], sp["H"], slots))
+        for _ in sp["passes"]:
+            launch_bytes.append(algorithmic_bytes(c, 2, sp["W"], sp["H"], slots))
     by_kind: dict[int, list] = {}
     for kd, ms, b in zip(kinds, med, launch_bytes):
         by_kind.setdefault(kd, []).append((ms, b))
-    names = {1: "k1_blocks", 2: "k2_level", 3: "k3_root"}
+    names = {1: "k1_blocks", 2: "k2_pass", 3: "k2_pass_root"}
     kernel_share = {names[kd]: sum(m for m, _ in v) for kd, v in by_kind.items()}
     dom = max(by_kind, key=lambda kd: sum(m for m, _ in by_kind[kd]))
     dom_ms = statistics.mean(m for m, _ in by_kind[dom])

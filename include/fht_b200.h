@@ -141,11 +141,12 @@ int fht_count_additions_tree(int w, int h, int strategy, uint64_t* result); /* o
 
 /* Host-only export of the schedule tables for one working orientation
  * (W slopes x H shifts) as JSON: blocks [x0, shape, depth], shapes {width,
- * steps, halo, step_offset, ops [dst, a, b, shift, extra]} and upper levels
- * {depth, ops [dst, a, b, r]}.  Needs no GPU; used by the CPU tests that
- * replay the schedule against the oracle.  Returns FHT_ERR_INVALID if `len`
- * is too small (then *needed holds the size). */
-int fht_schedule_json(int W, int H, int strategy, int block_width, char* buf, size_t len, size_t* needed);
+ * steps, halo, step_offset, ops [dst, a, b, shift, extra]} and the fused
+ * upper passes {levels, tiles, loads, step_offs, ops, stores}.  Needs no GPU;
+ * used by the CPU tests that replay the schedule against the oracle.
+ * Returns FHT_ERR_INVALID if `len` is too small (then *needed holds the size). */
+int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_levels, int tile_width, char* buf,
+                      size_t len, size_t* needed);
 
 /* Message of the last failed call on this thread ("" if none). */
 const char* fht_last_error(void);

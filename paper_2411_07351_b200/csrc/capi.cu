@@ -84,8 +84,7 @@ struct DevTables {
     const ShapeHdr* shapes = nullptr;
     const int* step_offs = nullptr;
     const int4* k1_ops = nullptr;
-    std::vector<const int4*> level_ops;
-    std::vector<int> level_nops, level_depth;
+    std::vector<fhtb::PassDev> passes;  // device pointers; S/L filled by create_plan
     int max_ops = 0, max_steps = 0;
 };
 
@@ -93,7 +92,7 @@ struct Group {
     QuadSet qs{};
     SubPlan sp;
     DevTables dt;
-    int ld = 0, S = 0, sr = 0;
+    int ld = 0, S = 0, sr = 0, nbuf = 0;
     size_t slot_bytes = 0;
 };
 
@@ -174,13 +173,24 @@ void upload(Group& g) {
     const size_t o_shapes = put(shapes.data(), shapes.size() * sizeof(ShapeHdr));
     const size_t o_steps = put(step_offs.data(), step_offs.size() * sizeof(int));
     const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(int4));
-    std::vector<size_t> o_levels;
-    for (const auto& lvl : sp.levels) {
-        std::vector<int4> ops;
-        for (const auto& op : lvl.ops) ops.push_back(make_int4(op.dst, op.a, op.b, op.r));
-        o_levels.push_back(put(ops.data(), ops.size() * sizeof(int4)));
-        g.dt.level_nops.push_back(static_cast<int>(ops.size()));
-        g.dt.level_depth.push_back(lvl.depth);
+    struct PassOff {
+        size_t tiles, loads, steps, ops, stores;
+    };
+    std::vector<PassOff> o_passes;
+    for (const auto& ps : sp.passes) {
+        static_assert(sizeof(fhtb::PassTile) == sizeof(fhtb::PassTileDev), "tile layout");
+        static_assert(sizeof(fhtb::PassOp) == sizeof(fhtb::PassOpDev), "op layout");
+        PassOff o{};
+        o.tiles = put(ps.tiles.data(), ps.tiles.size() * sizeof(fhtb::PassTile));
+        std::vector<int4> loads;
+        for (const auto& l : ps.loads) loads.push_back(make_int4(l.gcol, l.slot, l.off, l.ext));
+        o.loads = put(loads.data(), loads.size() * sizeof(int4));
+        o.steps = put(ps.step_offs.data(), ps.step_offs.size() * sizeof(int));
+        o.ops = put(ps.ops.data(), ps.ops.size() * sizeof(fhtb::PassOp));
+        std::vector<int2> stores;
+        for (const auto& st : ps.stores) stores.push_back(make_int2(st.slot, st.gcol));
+        o.stores = put(stores.data(), stores.size() * sizeof(int2));
+        o_passes.push_back(o);
     }
     blob.resize(blob.size() + 16);
     cuda_check(cudaMalloc(&g.dt.blob, blob.size()), "cudaMalloc(plan tables)");
@@ -190,13 +200,35 @@ void upload(Group& g) {
     g.dt.shapes = reinterpret_cast<const ShapeHdr*>(base + o_shapes);
     g.dt.step_offs = reinterpret_cast<const int*>(base + o_steps);
     g.dt.k1_ops = reinterpret_cast<const int4*>(base + o_k1);
-    for (size_t o : o_levels) g.dt.level_ops.push_back(reinterpret_cast<const int4*>(base + o));
+    for (size_t i = 0; i < o_passes.size(); ++i) {
+        const PassOff& o = o_passes[i];
+        fhtb::PassDev d{};
+        d.tiles = reinterpret_cast<const fhtb::PassTileDev*>(base + o.tiles);
+        d.loads = reinterpret_cast<const int4*>(base + o.loads);
+        d.step_offs = reinterpret_cast<const int*>(base + o.steps);
+        d.ops = reinterpret_cast<const fhtb::PassOpDev*>(base + o.ops);
+        d.stores = reinterpret_cast<const int2*>(base + o.stores);
+        d.ntiles = static_cast<int>(sp.passes[i].tiles.size());
+        d.max_slots = sp.passes[i].max_slots;
+        g.dt.passes.push_back(d);
+    }
 }
 
-int block_width_default() {
-    if (const char* e = std::getenv("FHT_BLOCK_WIDTH")) return std::max(1, std::min(64, std::atoi(e)));
-    return 32;
+int env_int(const char* name, int def, int lo, int hi) {
+    if (const char* e = std::getenv(name)) return std::max(lo, std::min(hi, std::atoi(e)));
+    return def;
 }
+
+// Rows per K2 row tile for a pass: as many as fit `budget` bytes of shared
+// memory (max_slots slots of S + max_ext rows), capped at H; multiples of 32.
+int pass_rows(const fhtb::FusedPass& ps, int H, size_t esz, size_t budget) {
+    const long cap = static_cast<long>(budget / (esz * static_cast<size_t>(std::max(1, ps.max_slots)))) - ps.max_ext - 1;
+    if (cap >= H) return H;
+    if (cap < 32) return static_cast<int>(std::max(0L, cap));
+    return static_cast<int>(cap / 32 * 32);
+}
+
+int block_width_default() { return env_int("FHT_BLOCK_WIDTH", 32, 1, 64); }
 
 fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, int mask, int batch, int layout,
                         int device) {
@@ -243,7 +275,19 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     for (auto& [horizontal, codes] : orient) {
         auto g = std::make_unique<Group>();
         const int W = horizontal ? w : h, H = horizontal ? h : w;
-        g->sp = SubPlan::build(W, H, strategy, bw);
+        // Fused-pass tiles: shrink the tile width until every pass gets a
+        // reasonable row tile in the shared-memory budget.
+        const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 100, 16, 220)) * 1024;
+        const int levels = env_int("FHT_PASS_LEVELS", 4, 1, 8);
+        int tw = env_int("FHT_TILE_WIDTH", 32, 1, 4096);
+        for (;;) {
+            g->sp = SubPlan::build(W, H, strategy, bw, levels, tw);
+            bool ok = true;
+            for (const auto& ps : g->sp.passes) ok = ok && pass_rows(ps, H, acc_sz, budget) >= std::min(H, 32);
+            if (ok) break;
+            if (tw == 1) throw FhtError(FHT_ERR_INTERNAL, "fused pass does not fit shared memory");
+            tw = std::max(1, tw / 2);
+        }
         g->qs.n = static_cast<int>(codes.size());
         for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
         g->ld = round_up(H, acc_sz == 8 ? 16 : 32);
@@ -252,8 +296,15 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         g->S = S;
         g->sr = S + g->sp.max_halo;
         if ((g->sr & 1) == 0) g->sr += 1;
-        g->slot_bytes = g->sp.root_is_block ? 0 : 2 * static_cast<size_t>(W) * g->ld * acc_sz;
+        g->nbuf = g->sp.root_is_block ? 0 : (g->sp.passes.size() > 1 ? 2 : 1);
+        g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
         upload(*g);
+        for (size_t i = 0; i < g->dt.passes.size(); ++i) {
+            auto& d = g->dt.passes[i];
+            d.S = pass_rows(g->sp.passes[i], H, acc_sz, budget);
+            d.L = d.S + g->sp.passes[i].max_ext;
+            if ((d.L & 1) == 0) d.L += 1;
+        }
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
@@ -272,7 +323,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     p->ws_bytes = max_slot_bytes * static_cast<size_t>(chunk);
     const int nchunks = (batch + chunk - 1) / chunk;
     int per_chunk = 0;
-    for (auto& g : p->groups) per_chunk += 1 + (g->sp.root_is_block ? 0 : static_cast<int>(g->sp.levels.size()));
+    for (auto& g : p->groups) per_chunk += 1 + static_cast<int>(g->sp.passes.size());
     p->launches = per_chunk * nchunks;
     return p.release();
 }
@@ -312,11 +363,10 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.k1_max_width = g.sp.max_block_width;
             L.k1_sr = g.sr;
             L.root_is_block = g.sp.root_is_block;
-            L.nlevels = static_cast<int>(g.dt.level_ops.size());
-            L.level_ops = g.dt.level_ops.data();
-            L.level_nops = g.dt.level_nops.data();
-            L.level_depth = g.dt.level_depth.data();
+            L.npasses = static_cast<int>(g.dt.passes.size());
+            L.passes = g.dt.passes.data();
             L.ws = ws;
+            L.nbuf = g.nbuf;
             for (int q = 0; q < 4; ++q) L.out.ptr[q] = d_out[q];
             L.out.img_stride = out_stride;
             L.out.layout = p->layout;
@@ -459,7 +509,11 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
             const Group& g = *plan->groups[i];
             o << (i ? "," : "") << "{\"quadrants\":[";
             for (int k = 0; k < g.qs.n; ++k) o << (k ? "," : "") << g.qs.code[k];
-            o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"plan\":" << g.sp.describe() << "}";
+            o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"nbuf\":" << g.nbuf
+              << ",\"pass_rows\":[";
+            for (size_t k = 0; k < g.dt.passes.size(); ++k)
+                o << (k ? "," : "") << "[" << g.dt.passes[k].S << "," << g.dt.passes[k].L << "]";
+            o << "],\"plan\":" << g.sp.describe() << "}";
         }
         o << "]}";
         const std::string s = o.str();
@@ -568,9 +622,10 @@ int fht_count_additions_tree(int w, int h, int strategy, uint64_t* result) {
     });
 }
 
-int fht_schedule_json(int W, int H, int strategy, int block_width, char* buf, size_t len, size_t* needed) {
+int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_levels, int tile_width, char* buf,
+                      size_t len, size_t* needed) {
     return guarded([&] {
-        const SubPlan sp = SubPlan::build(W, H, strategy, block_width);
+        const SubPlan sp = SubPlan::build(W, H, strategy, block_width, pass_levels, tile_width);
         std::ostringstream o;
         o << "{\"W\":" << sp.W << ",\"H\":" << sp.H << ",\"root_is_block\":" << (sp.root_is_block ? 1 : 0)
           << ",\"additions\":" << sp.additions << ",\"blocks\":[";
@@ -588,13 +643,31 @@ int fht_schedule_json(int W, int H, int strategy, int block_width, char* buf, si
                   << "," << s.extra[k] << "]";
             o << "]}";
         }
-        o << "],\"levels\":[";
-        for (size_t i = 0; i < sp.levels.size(); ++i) {
-            o << (i ? "," : "") << "{\"depth\":" << sp.levels[i].depth << ",\"ops\":[";
-            for (size_t k = 0; k < sp.levels[i].ops.size(); ++k) {
-                const auto& op = sp.levels[i].ops[k];
-                o << (k ? "," : "") << "[" << op.dst << "," << op.a << "," << op.b << "," << op.r << "]";
+        o << "],\"passes\":[";
+        for (size_t i = 0; i < sp.passes.size(); ++i) {
+            const auto& ps = sp.passes[i];
+            o << (i ? "," : "") << "{\"levels\":" << ps.levels << ",\"max_slots\":" << ps.max_slots
+              << ",\"max_ext\":" << ps.max_ext << ",\"tiles\":[";
+            for (size_t k = 0; k < ps.tiles.size(); ++k) {
+                const auto& t = ps.tiles[k];
+                o << (k ? "," : "") << "[" << t.load_beg << "," << t.load_cnt << "," << t.step_beg << "," << t.nsteps << ","
+                  << t.store_beg << "," << t.store_cnt << "," << t.nslots << "," << t.max_ext << "]";
             }
+            o << "],\"loads\":[";
+            for (size_t k = 0; k < ps.loads.size(); ++k)
+                o << (k ? "," : "") << "[" << ps.loads[k].gcol << "," << ps.loads[k].slot << "," << ps.loads[k].off << ","
+                  << ps.loads[k].ext << "]";
+            o << "],\"step_offs\":[";
+            for (size_t k = 0; k < ps.step_offs.size(); ++k) o << (k ? "," : "") << ps.step_offs[k];
+            o << "],\"ops\":[";
+            for (size_t k = 0; k < ps.ops.size(); ++k) {
+                const auto& op = ps.ops[k];
+                o << (k ? "," : "") << "[" << op.dst << "," << op.a << "," << op.b << "," << op.ad << "," << op.bd << ","
+                  << op.ext << "]";
+            }
+            o << "],\"stores\":[";
+            for (size_t k = 0; k < ps.stores.size(); ++k)
+                o << (k ? "," : "") << "[" << ps.stores[k].slot << "," << ps.stores[k].gcol << "]";
             o << "]}";
         }
         o << "]}";

@@ -56,6 +56,10 @@ __device__ __forceinline__ int to_bits(T v) {
     else return static_cast<int>(v);
 }
 
+__device__ __forceinline__ size_t k1_ops_offset_dev(size_t esz, int max_width, int sr) {
+    return (2 * static_cast<size_t>(max_width) * sr * esz + 15) / 16 * 16;
+}
+
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
 template <class In, class Acc, class Out>
@@ -63,16 +67,16 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
     const In* __restrict__ img, int img_w, int img_h, long long img_stride, int img0, QuadSet qs, int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
     const int* __restrict__ step_offs, const int4* __restrict__ ops, int max_width, int sr, int max_ops,
-    Acc* __restrict__ ws, bool root_is_block, OutDesc out) {
+    Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);
     Acc* buf1 = buf0 + (size_t)max_width * sr;
-    int4* sops = reinterpret_cast<int4*>(buf1 + (size_t)max_width * sr);
+    int4* sops = reinterpret_cast<int4*>(smem_raw + k1_ops_offset_dev(sizeof(Acc), max_width, sr));
     int* soffs = reinterpret_cast<int*>(sops + max_ops);
 
     const int tid = threadIdx.x;
     const int4 blk = blocks[blockIdx.y];
-    const int x0 = blk.x, depth = blk.z;
+    const int x0 = blk.x;
     const ShapeHdr hdr = shapes[blk.y];
     const int wb = hdr.width, nsteps = hdr.nsteps;
     const int R = S + hdr.halo;
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
     // Store the block root's S rows (values of local depth 0 live in buf0).
     const int rows_out = min(S, H - s0);
     if (!root_is_block) {
-        Acc* __restrict__ dstw = ws + (size_t)slot * 2 * W * ld + (size_t)(depth & 1) * W * ld;
+        Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;  // pass 0 output: buffer 0
         const int n = wb * rows_out;
         for (int k = tid; k < n; k += kThreads) {
             const int i = k % rows_out, c = k / rows_out;
@@ -154,94 +158,89 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
 }
 
 // ------------------------------------------------------------------- K2
-// grid: x = op (output column), y = chunk of 4*kThreads rows, z = slot.
-// src/dst are the two ping-pong buffers of the slot, or (to_out) the
-// native-layout output.
-template <class Acc, class Out, bool VEC>
-__global__ void __launch_bounds__(kThreads) k2_level(const int4* __restrict__ ops, const Acc* __restrict__ src_buf,
-                                                      Acc* __restrict__ dst_buf, long long slot_elems, int H, int ld,
-                                                      bool to_out, OutDesc out, QuadSet qs, int img0) {
-    const int4 op = ops[blockIdx.x];
-    const int slot = blockIdx.z;
-    const Acc* __restrict__ src = src_buf + (size_t)slot * slot_elems;
-    const Acc* __restrict__ A = src + (size_t)op.y * ld;
-    const Acc* __restrict__ B = src + (size_t)op.z * ld;
-    const int r = op.w;
-    const int s = (blockIdx.y * kThreads + threadIdx.x) * 4;
-    if (s >= H) return;
-    Out* __restrict__ D;
-    if (!to_out) {
-        D = reinterpret_cast<Out*>(dst_buf) + (size_t)slot * slot_elems + (size_t)op.x * ld;
-    } else {
-        const int nq = qs.n;
-        D = reinterpret_cast<Out*>(out.ptr[qs.code[slot % nq]]) + (size_t)(img0 + slot / nq) * out.img_stride +
-            (size_t)op.x * H;
-    }
-    Acc v[4];
-    if (VEC && s + 3 < H) {
-        if constexpr (sizeof(Acc) == 4) {
-            const int4 a4 = *reinterpret_cast<const int4*>(A + s);
-            v[0] = from_bits<Acc>(a4.x);
-            v[1] = from_bits<Acc>(a4.y);
-            v[2] = from_bits<Acc>(a4.z);
-            v[3] = from_bits<Acc>(a4.w);
-        } else {
-            const longlong2 a0 = *reinterpret_cast<const longlong2*>(A + s);
-            const longlong2 a1 = *reinterpret_cast<const longlong2*>(A + s + 2);
-            v[0] = a0.x, v[1] = a0.y, v[2] = a1.x, v[3] = a1.y;
-        }
-        int j = wrap_once(s + r, H);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            v[e] = v[e] + B[j];
-            j = wrap_once(j + 1, H);
-        }
-        if constexpr (VEC && std::is_same<Acc, Out>::value && sizeof(Acc) == 4) {
-            if (!to_out) {
-                *reinterpret_cast<int4*>(D + s) =
-                    make_int4(to_bits(v[0]), to_bits(v[1]), to_bits(v[2]), to_bits(v[3]));
-                return;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) D[s + e] = static_cast<Out>(v[e]);
-    } else {
-        int j = wrap_once(s + r, H);
-        for (int e = 0; e < 4 && s + e < H; ++e) {
-            D[s + e] = static_cast<Out>(A[s + e] + B[j]);
-            j = wrap_once(j + 1, H);
-        }
-    }
-}
-
-// ------------------------------------------------------------------- K3
-// Root level + transpose into hough[s*W + t].  grid: x = 32-slope tile,
-// y = 32-shift tile, z = slot.  Block 32 x 8.
+// One fused upper pass.  grid: x = row tile (S rows), y = tile (G slopes of
+// one band node), z = slot (image * nq + quadrant index).  A tile is a small
+// program (plan.cpp build_tile): load the row windows of the frontier columns
+// it depends on, run its merge ops level by level in shared memory (slot-
+// major, row capacity L), then store its G columns -- into the other
+// workspace buffer, or (root pass) straight into the output in the
+// reference layout hough[s*W + t] (transform.cpp:80-83).
 template <class Acc, class Out>
-__global__ void __launch_bounds__(256) k3_root(const int4* __restrict__ ops, const Acc* __restrict__ ws, int W,
-                                                int H, int ld, int src_par, OutDesc out, QuadSet qs, int img0) {
-    __shared__ Acc tile[32][33];
-    const int lane = threadIdx.x, ty = threadIdx.y;
-    const int t0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+__global__ void __launch_bounds__(kThreads) k2_pass(PassDev ps, const Acc* __restrict__ src,
+                                                     Acc* __restrict__ dst, long long slot_elems, int W, int H,
+                                                     int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Acc* sm = reinterpret_cast<Acc*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kWarps = kThreads / 32;
+    const PassTileDev tile = ps.tiles[blockIdx.y];
+    const int S = ps.S, L = ps.L;
+    const int s0 = blockIdx.x * S;
     const int slot = blockIdx.z;
-    const Acc* __restrict__ src = ws + (size_t)slot * 2 * W * ld + (size_t)src_par * W * ld;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int tl = ty + 8 * j, t = t0 + tl, s = s0 + lane;
-        if (t < W && s < H) {
-            const int4 op = ops[t];
-            const int jb = wrap_once(s + op.w, H);
-            tile[tl][lane] = src[(size_t)op.y * ld + s] + src[(size_t)op.z * ld + jb];
+    const Acc* __restrict__ in = src + (size_t)slot * slot_elems;
+
+    // 1. windows of the input columns
+    for (int l = warp; l < tile.load_cnt; l += kWarps) {
+        const int4 ld4 = ps.loads[tile.load_beg + l];
+        const Acc* __restrict__ col = in + (size_t)ld4.x * ld;
+        Acc* __restrict__ d = sm + (size_t)ld4.y * L;
+        const int n = S + ld4.w;
+        int y = wrap_any(s0 + ld4.z + lane, H);
+        for (int i = lane; i < n; i += 32) {
+            d[i] = col[y];
+            y += 32;
+            if (y >= H) y = wrap_any(y, H);
+        }
+    }
+    // 2. merge levels
+    for (int k = 0; k < tile.nsteps; ++k) {
+        __syncthreads();
+        const int o_beg = ps.step_offs[tile.step_beg + k], o_end = ps.step_offs[tile.step_beg + k + 1];
+        for (int o = o_beg + warp; o < o_end; o += kWarps) {
+            const PassOpDev op = ps.ops[o];
+            const Acc* a = sm + (size_t)op.a * L + op.ad;
+            Acc* d = sm + (size_t)op.dst * L;
+            const int n = S + op.ext;
+            if (op.b >= 0) {
+                const Acc* b = sm + (size_t)op.b * L + op.bd;
+                for (int i = lane; i < n; i += 32) d[i] = a[i] + b[i];
+            } else {
+                for (int i = lane; i < n; i += 32) d[i] = a[i];
+            }
         }
     }
     __syncthreads();
-    const int nq = qs.n;
-    Out* __restrict__ o =
-        reinterpret_cast<Out*>(out.ptr[qs.code[slot % nq]]) + (size_t)(img0 + slot / nq) * out.img_stride;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int sl = ty + 8 * j, s = s0 + sl, t = t0 + lane;
-        if (s < H && t < W) o[(size_t)s * W + t] = static_cast<Out>(tile[lane][sl]);
+    // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)
+    const int rows = min(S, H - s0);
+    if (!final_pass) {
+        Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
+        for (int c = warp; c < tile.store_cnt; c += kWarps) {
+            const int2 st = ps.stores[tile.store_beg + c];
+            const Acc* sv = sm + (size_t)st.x * L;
+            Acc* __restrict__ dcol = o + (size_t)st.y * ld + s0;
+            for (int i = lane; i < rows; i += 32) dcol[i] = sv[i];
+        }
+    } else {
+        const int nq = qs.n;
+        Out* __restrict__ o =
+            reinterpret_cast<Out*>(out.ptr[qs.code[slot % nq]]) + (size_t)(img0 + slot / nq) * out.img_stride;
+        const int nc = tile.store_cnt;
+        if (out.layout == 0) {
+            // stores of a tile are consecutive slopes: write rows of nc contiguous t
+            const int t0 = ps.stores[tile.store_beg].y;
+            for (int k = tid; k < nc * rows; k += kThreads) {
+                const int c = k % nc, i = k / nc;
+                const int2 st = ps.stores[tile.store_beg + c];
+                o[(size_t)(s0 + i) * W + t0 + c] = static_cast<Out>(sm[(size_t)st.x * L + i]);
+            }
+        } else {
+            for (int c = warp; c < nc; c += kWarps) {
+                const int2 st = ps.stores[tile.store_beg + c];
+                const Acc* sv = sm + (size_t)st.x * L;
+                Out* __restrict__ dcol = o + (size_t)st.y * H + s0;
+                for (int i = lane; i < rows; i += 32) dcol[i] = static_cast<Out>(sv[i]);
+            }
+        }
     }
 }
 
@@ -273,52 +272,42 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
     k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride, g.img0, g.qs,
                                    g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs, g.k1_ops, g.k1_max_width,
-                                   g.k1_sr, g.k1_max_ops, ws, g.root_is_block, g.out);
+                                   g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out);
     ++launches;
     if (hook) hook(ctx, 1);
     if (g.root_is_block) return launches;
-    const bool vec = (g.ld % 4 == 0);
-    for (int l = 0; l < g.nlevels; ++l) {
-        const int d = g.level_depth[l];
-        const int src_par = (d + 1) & 1, dst_par = d & 1;
-        const long long slot_elems = 2LL * g.W * g.ld;
-        const Acc* SRC = ws + (size_t)src_par * g.W * g.ld;
-        Acc* DST = ws + (size_t)dst_par * g.W * g.ld;
-        if (d > 0 || g.out.layout == 1) {
-            const bool to_out = (d == 0);
-            dim3 g2(g.level_nops[l], (g.H + 4 * kThreads - 1) / (4 * kThreads), nslots);
-            if (!to_out) {
-                if (vec)
-                    k2_level<Acc, Acc, true><<<g2, kThreads, 0, st>>>(g.level_ops[l], SRC, DST, slot_elems, g.H, g.ld,
-                                                                     false, g.out, g.qs, g.img0);
-                else
-                    k2_level<Acc, Acc, false><<<g2, kThreads, 0, st>>>(g.level_ops[l], SRC, DST, slot_elems, g.H, g.ld,
-                                                                      false, g.out, g.qs, g.img0);
-            } else {
-                if (vec)
-                    k2_level<Acc, Out, true><<<g2, kThreads, 0, st>>>(g.level_ops[l], SRC, DST, slot_elems, g.H, g.ld,
-                                                                     true, g.out, g.qs, g.img0);
-                else
-                    k2_level<Acc, Out, false><<<g2, kThreads, 0, st>>>(g.level_ops[l], SRC, DST, slot_elems, g.H, g.ld,
-                                                                      true, g.out, g.qs, g.img0);
-            }
-        } else {
-            dim3 g3((g.W + 31) / 32, (g.H + 31) / 32, nslots);
-            k3_root<Acc, Out><<<g3, dim3(32, 8), 0, st>>>(g.level_ops[l], ws, g.W, g.H, g.ld, src_par, g.out, g.qs,
-                                                          g.img0);
-        }
+    const long long slot_elems = (long long)g.nbuf * g.W * g.ld;
+    for (int p = 0; p < g.npasses; ++p) {
+        const PassDev& ps = g.passes[p];
+        const bool final_pass = (p == g.npasses - 1);
+        const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
+        Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
+        const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L);
+        auto k2 = k2_pass<Acc, Out>;
+        cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+        dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
+        k2<<<g2, kThreads, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
         ++launches;
-        if (hook) hook(ctx, (d > 0 || g.out.layout == 1) ? 2 : 3);
+        if (hook) hook(ctx, final_pass ? 3 : 2);
     }
     return launches;
 }
 
 }  // namespace
 
-size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps) {
+static size_t k1_ops_offset(int acc_dtype, int max_width, int sr) {
     const size_t esz = acc_dtype == kI64 ? 8 : 4;
-    return 2 * static_cast<size_t>(max_width) * sr * esz + static_cast<size_t>(max_ops) * sizeof(int4) +
+    return (2 * static_cast<size_t>(max_width) * sr * esz + 15) / 16 * 16;
+}
+
+size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps) {
+    return k1_ops_offset(acc_dtype, max_width, sr) + static_cast<size_t>(max_ops) * sizeof(int4) +
            static_cast<size_t>(max_steps + 1) * sizeof(int) + 16;
+}
+
+size_t k2_smem_bytes(int acc_dtype, int max_slots, int L) {
+    const size_t esz = acc_dtype == kI64 ? 8 : 4;
+    return static_cast<size_t>(max_slots) * L * esz;
 }
 
 int launch_group(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* ctx) {

@@ -35,6 +35,25 @@ struct ShapeHdr {
     int width, nsteps, op_base, step_base, halo, pad0, pad1, pad2;
 };
 
+// Device tables of one fused upper pass (see plan.hpp FusedPass).
+struct PassTileDev {
+    int load_beg, load_cnt, step_beg, nsteps, store_beg, store_cnt, nslots, max_ext;
+};
+struct PassOpDev {
+    int dst, a, b, ad, bd, ext, pad0, pad1;
+};
+struct PassDev {
+    const PassTileDev* tiles;
+    const int4* loads;  // gcol, slot, off, ext
+    const int* step_offs;
+    const PassOpDev* ops;
+    const int2* stores;  // slot, gcol
+    int ntiles;
+    int S;       // rows per row tile
+    int L;       // smem row capacity of a slot (>= S + max_ext, odd)
+    int max_slots;
+};
+
 struct GroupLaunch {
     // image
     const void* img;
@@ -56,20 +75,21 @@ struct GroupLaunch {
     const int4* k1_ops;
     int k1_max_ops, k1_max_steps, k1_max_width, k1_sr;
     bool root_is_block;
-    // upper levels, deepest first; the last is the root when !root_is_block
-    int nlevels;
-    const int4* const* level_ops;
-    const int* level_nops;
-    const int* level_depth;
-    // workspace: per slot two W x ld buffers
+    // fused upper passes (K2), in execution order; the last writes the root
+    int npasses;
+    const PassDev* passes;
+    // workspace: per slot nbuf (1 or 2) W x ld buffers
     void* ws;
+    int nbuf;
     OutDesc out;
 };
 
 size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps);
+size_t k2_smem_bytes(int acc_dtype, int max_slots, int L);
 // Launch every kernel of one orientation group / chunk on `stream`.
 // Returns the number of kernel launches, or -1 on an unsupported type combination.
-// `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1, 2 = K2, 3 = K3.
+// `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1, 2 = K2
+// (fused upper pass), 3 = K2 writing the root.
 typedef void (*LaunchHook)(void* ctx, int kind);
 int launch_group(const GroupLaunch& g, cudaStream_t stream, LaunchHook hook = nullptr, void* ctx = nullptr);
 

@@ -118,10 +118,167 @@ BlockShape build_shape(int wb, int strategy) {
 
 }  // namespace
 
-SubPlan SubPlan::build(int W, int H, int strategy, int block_width) {
+namespace {
+
+// One fused tile: the slopes [ta, tb) of band node X, whose inputs are the
+// frontier nodes below it.  Appends the program to `ps`.
+void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, const std::vector<int>& height,
+                int X, int ta, int tb, int H, FusedPass& ps) {
+    struct Entry {
+        int lo = 0, hi = 0;  // window rows [s0+lo, s0+hi+S): ext = hi - lo
+        int slot = -1;
+        int last_use = -1;   // last step reading it
+        bool seen = false;
+    };
+    // Entries per node: local column -> Entry (only needed columns).
+    std::vector<std::vector<Entry>> ent(nodes.size());
+    std::vector<int> order;  // nodes of the tile program, parents before children
+    auto touch = [&](int n) {
+        if (ent[static_cast<size_t>(n)].empty()) {
+            ent[static_cast<size_t>(n)].resize(static_cast<size_t>(nodes[static_cast<size_t>(n)].w));
+            order.push_back(n);
+        }
+    };
+    touch(X);
+    for (int t = ta; t < tb; ++t) {
+        Entry& e = ent[static_cast<size_t>(X)][static_cast<size_t>(t)];
+        e.seen = true;
+        e.lo = 0;
+        e.hi = 0;
+    }
+    for (size_t qi = 0; qi < order.size(); ++qi) {
+        const int n = order[qi];
+        if (front[static_cast<size_t>(n)]) continue;  // input node
+        const Node& nd = nodes[static_cast<size_t>(n)];
+        const int c0 = nd.child[0], c1 = nd.child[1];
+        const int w = nd.w, w0 = nodes[static_cast<size_t>(c0)].w, w1 = w - w0;
+        touch(c0);
+        touch(c1);
+        for (int t = 0; t < w; ++t) {
+            const Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+            if (!e.seen) continue;
+            const int t0 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), w - 1));
+            const int t1 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), w - 1));
+            const int r = (t - t1) % H;
+            Entry& a = ent[static_cast<size_t>(c0)][static_cast<size_t>(t0)];
+            Entry& b = ent[static_cast<size_t>(c1)][static_cast<size_t>(t1)];
+            if (!a.seen) a.lo = e.lo, a.hi = e.hi, a.seen = true;
+            a.lo = std::min(a.lo, e.lo);
+            a.hi = std::max(a.hi, e.hi);
+            if (!b.seen) b.lo = e.lo + r, b.hi = e.hi + r, b.seen = true;
+            b.lo = std::min(b.lo, e.lo + r);
+            b.hi = std::max(b.hi, e.hi + r);
+        }
+    }
+    // Steps by height above the frontier; last use of every entry.
+    const int hx = height[static_cast<size_t>(X)];
+    std::vector<std::vector<int>> step_nodes(static_cast<size_t>(std::max(hx, 0)));
+    for (int n : order)
+        if (!front[static_cast<size_t>(n)]) step_nodes[static_cast<size_t>(height[static_cast<size_t>(n)] - 1)].push_back(n);
+    for (int j = 0; j < hx; ++j)
+        for (int n : step_nodes[static_cast<size_t>(j)]) {
+            const Node& nd = nodes[static_cast<size_t>(n)];
+            const int c0 = nd.child[0], c1 = nd.child[1];
+            const int w = nd.w, w0 = nodes[static_cast<size_t>(c0)].w, w1 = w - w0;
+            for (int t = 0; t < w; ++t) {
+                if (!ent[static_cast<size_t>(n)][static_cast<size_t>(t)].seen) continue;
+                const int t0 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), w - 1));
+                const int t1 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), w - 1));
+                ent[static_cast<size_t>(c0)][static_cast<size_t>(t0)].last_use = j;
+                ent[static_cast<size_t>(c1)][static_cast<size_t>(t1)].last_use = j;
+            }
+        }
+    // Slot allocation: loads first, then each step's outputs from slots freed
+    // by earlier steps (a slot is never reused within the step that frees it).
+    PassTile tile{};
+    tile.load_beg = static_cast<int>(ps.loads.size());
+    tile.step_beg = static_cast<int>(ps.step_offs.size());
+    tile.nsteps = hx;
+    tile.store_beg = static_cast<int>(ps.stores.size());
+    int next_slot = 0, max_ext = 0;
+    std::vector<int> free_slots;
+    for (int n : order) {
+        if (!front[static_cast<size_t>(n)]) continue;
+        const Node& nd = nodes[static_cast<size_t>(n)];
+        for (int t = 0; t < nd.w; ++t) {
+            Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+            if (!e.seen) continue;
+            e.slot = next_slot++;
+            ps.loads.push_back({nd.x0 + t, e.slot, e.lo, e.hi - e.lo});
+            ps.loaded_cells += e.hi - e.lo;
+            max_ext = std::max(max_ext, e.hi - e.lo);
+        }
+    }
+    tile.load_cnt = static_cast<int>(ps.loads.size()) - tile.load_beg;
+    std::vector<std::pair<int, int>> live;  // (node, col) computed so far, for freeing
+    for (int n : order)
+        if (front[static_cast<size_t>(n)])
+            for (int t = 0; t < nodes[static_cast<size_t>(n)].w; ++t)
+                if (ent[static_cast<size_t>(n)][static_cast<size_t>(t)].seen) live.push_back({n, t});
+    for (int j = 0; j < hx; ++j) {
+        ps.step_offs.push_back(static_cast<int>(ps.ops.size()));
+        for (int n : step_nodes[static_cast<size_t>(j)]) {
+            const Node& nd = nodes[static_cast<size_t>(n)];
+            const int c0 = nd.child[0], c1 = nd.child[1];
+            const int w = nd.w, w0 = nodes[static_cast<size_t>(c0)].w, w1 = w - w0;
+            for (int t = 0; t < w; ++t) {
+                Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+                if (!e.seen) continue;
+                const int t0 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), w - 1));
+                const int t1 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), w - 1));
+                const int r = (t - t1) % H;
+                const Entry& a = ent[static_cast<size_t>(c0)][static_cast<size_t>(t0)];
+                const Entry& b = ent[static_cast<size_t>(c1)][static_cast<size_t>(t1)];
+                if (free_slots.empty()) {
+                    e.slot = next_slot++;
+                } else {
+                    e.slot = free_slots.back();
+                    free_slots.pop_back();
+                }
+                PassOp op{};
+                op.dst = e.slot;
+                op.a = a.slot;
+                op.b = b.slot;
+                op.ad = e.lo - a.lo;
+                op.bd = e.lo + r - b.lo;
+                op.ext = e.hi - e.lo;
+                if (op.ad < 0 || op.bd < 0 || op.ad + op.ext > a.hi - a.lo || op.bd + op.ext > b.hi - b.lo)
+                    throw std::logic_error("fused tile window derivation failed");
+                ps.ops.push_back(op);
+                max_ext = std::max(max_ext, op.ext);
+                live.push_back({n, t});
+            }
+        }
+        // free the slots whose last consumer was this step (usable from step j+1)
+        std::vector<std::pair<int, int>> keep;
+        for (auto [n, t] : live) {
+            const Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+            if (n != X && e.last_use == j)
+                free_slots.push_back(e.slot);
+            else
+                keep.push_back({n, t});
+        }
+        live.swap(keep);
+    }
+    ps.step_offs.push_back(static_cast<int>(ps.ops.size()));
+    const Node& xn = nodes[static_cast<size_t>(X)];
+    for (int t = ta; t < tb; ++t) ps.stores.push_back({ent[static_cast<size_t>(X)][static_cast<size_t>(t)].slot, xn.x0 + t});
+    tile.store_cnt = tb - ta;
+    tile.nslots = next_slot;
+    tile.max_ext = max_ext;
+    ps.max_slots = std::max(ps.max_slots, next_slot);
+    ps.max_ext = std::max(ps.max_ext, max_ext);
+    ps.tiles.push_back(tile);
+}
+
+}  // namespace
+
+SubPlan SubPlan::build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width) {
     if (W < 1 || H < 1) throw std::invalid_argument("fht2d: image is empty");
     if (strategy != kSimple && strategy != kTweaked) throw std::invalid_argument("unknown split strategy");
     if (block_width < 1 || block_width > 64) throw std::invalid_argument("block width must lie in [1, 64]");
+    if (pass_levels < 1 || pass_levels > 8) throw std::invalid_argument("pass levels must lie in [1, 8]");
+    if (tile_width < 1) throw std::invalid_argument("tile width must be positive");
     SubPlan p;
     p.W = W;
     p.H = H;
@@ -132,8 +289,9 @@ SubPlan SubPlan::build(int W, int H, int strategy, int block_width) {
     std::vector<Node> nodes;
     build_tree(nodes, 0, W, 0, strategy, block_width);
     std::map<int, int> shape_of_width;
-    int max_upper_depth = -1;
-    for (const Node& n : nodes) {
+    std::vector<char> front(nodes.size(), 0);
+    for (size_t i = 0; i < nodes.size(); ++i) {
+        const Node& n = nodes[i];
         if (n.w <= block_width) {
             auto it = shape_of_width.find(n.w);
             if (it == shape_of_width.end()) {
@@ -141,25 +299,51 @@ SubPlan SubPlan::build(int W, int H, int strategy, int block_width) {
                 p.shapes.push_back(build_shape(n.w, strategy));
             }
             p.blocks.push_back({n.x0, it->second, n.depth});
-        } else {
-            max_upper_depth = std::max(max_upper_depth, n.depth);
+            front[i] = 1;
+            p.tree_depth = std::max(p.tree_depth, n.depth + p.shapes[static_cast<size_t>(it->second)].depth);
         }
     }
     p.root_is_block = (W <= block_width);
-    for (int d = max_upper_depth; d >= 0; --d) {
-        UpperLevel lvl;
-        lvl.depth = d;
-        for (const Node& n : nodes) {
-            if (n.depth != d || n.w <= block_width) continue;
-            node_ops(n, nodes[static_cast<size_t>(n.child[0])], lvl.ops);
-        }
-        for (Op& op : lvl.ops) op.r %= H;  // transform.cpp:49
-        std::sort(lvl.ops.begin(), lvl.ops.end(), [](const Op& a, const Op& b) { return a.dst < b.dst; });
-        p.levels.push_back(std::move(lvl));
-    }
     for (const BlockShape& s : p.shapes) {
         p.max_block_width = std::max(p.max_block_width, s.width);
         p.max_halo = std::max(p.max_halo, s.halo);
+    }
+    // Parent pointers (nodes are in preorder: children follow their parent).
+    std::vector<int> parent(nodes.size(), -1);
+    for (size_t i = 0; i < nodes.size(); ++i)
+        for (int c : nodes[i].child)
+            if (c >= 0) parent[static_cast<size_t>(c)] = static_cast<int>(i);
+    // Bands of <= pass_levels levels above the current frontier.
+    while (!front[0]) {
+        std::vector<char> below(nodes.size(), 0);
+        for (size_t i = 1; i < nodes.size(); ++i) {
+            const size_t pa = static_cast<size_t>(parent[i]);
+            below[i] = below[pa] || front[pa];
+        }
+        std::vector<int> height(nodes.size(), 0);
+        for (size_t ii = nodes.size(); ii-- > 0;) {
+            if (below[ii] || front[ii]) continue;
+            const Node& n = nodes[ii];
+            height[ii] = 1 + std::max(height[static_cast<size_t>(n.child[0])], height[static_cast<size_t>(n.child[1])]);
+        }
+        const int U = height[0];
+        const int npass = (U + pass_levels - 1) / pass_levels;
+        const int k = (U + npass - 1) / npass;
+        std::vector<char> nfront(nodes.size(), 0);
+        FusedPass ps;
+        ps.tile_width = tile_width;
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            if (below[i]) continue;
+            const bool top = (i == 0) || height[static_cast<size_t>(parent[i])] > k;
+            if (height[i] > k || !top) continue;
+            nfront[i] = 1;
+            ps.levels = std::max(ps.levels, height[i]);
+            const int w = nodes[i].w;
+            for (int ta = 0; ta < w; ta += tile_width)
+                build_tile(nodes, front, height, static_cast<int>(i), ta, std::min(w, ta + tile_width), H, ps);
+        }
+        p.passes.push_back(std::move(ps));
+        front.swap(nfront);
     }
     return p;
 }
@@ -168,15 +352,20 @@ std::string SubPlan::describe() const {
     std::ostringstream o;
     o << "{\"W\":" << W << ",\"H\":" << H << ",\"strategy\":" << strategy << ",\"block_width\":" << block_width
       << ",\"root_is_block\":" << (root_is_block ? "true" : "false") << ",\"additions\":" << additions
-      << ",\"max_halo\":" << max_halo << ",\"shapes\":[";
+      << ",\"tree_depth\":" << tree_depth << ",\"max_halo\":" << max_halo << ",\"shapes\":[";
     for (size_t i = 0; i < shapes.size(); ++i) {
         const BlockShape& s = shapes[i];
         o << (i ? "," : "") << "{\"width\":" << s.width << ",\"steps\":" << s.depth << ",\"halo\":" << s.halo
           << ",\"ops\":" << s.ops.size() << "}";
     }
-    o << "],\"blocks\":" << blocks.size() << ",\"levels\":[";
-    for (size_t i = 0; i < levels.size(); ++i)
-        o << (i ? "," : "") << "{\"depth\":" << levels[i].depth << ",\"ops\":" << levels[i].ops.size() << "}";
+    o << "],\"blocks\":" << blocks.size() << ",\"passes\":[";
+    for (size_t i = 0; i < passes.size(); ++i) {
+        const FusedPass& f = passes[i];
+        o << (i ? "," : "") << "{\"levels\":" << f.levels << ",\"tiles\":" << f.tiles.size()
+          << ",\"tile_width\":" << f.tile_width << ",\"loads\":" << f.loads.size() << ",\"ops\":" << f.ops.size()
+          << ",\"stores\":" << f.stores.size() << ",\"max_slots\":" << f.max_slots << ",\"max_ext\":" << f.max_ext
+          << ",\"loaded_ext_cells\":" << f.loaded_cells << "}";
+    }
     o << "]}";
     return o.str();
 }

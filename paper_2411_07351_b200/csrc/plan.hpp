@@ -6,26 +6,30 @@
 //     OUT[t][s] = IN[t0][s] + IN[w0 + t1][(s + r) mod h]
 //     t0 = rhu(t (w0-1), w-1), t1 = rhu(t (w1-1), w-1), r = (t - t1) mod h
 // with rhu = round_half_up_ratio (split.hpp:53-57).  The SPEC allows any
-// evaluation order that is bit-identical; we evaluate it
-// level-order on the GPU:
+// evaluation order that is bit-identical.  We evaluate it in a
+// few HBM passes, each of which runs several tree levels in shared memory:
 //
-//  * "blocks": every maximal subtree of width <= block_width.  One CTA
-//    computes a whole block for a tile of S rows in shared memory (kernel
-//    K1), reading the input image in the quadrant's orientation.  A block's
-//    merge schedule depends only on its width, so it is a per-width "shape"
-//    table of (dst, a, b, shift) ops in block-local columns, with b = -1
-//    meaning "carry a leaf column one level up".  The rows a tile must load
-//    (the halo) are derived exactly from the tables by propagating the
-//    shifts backwards -- never assumed.
-//  * "upper levels": every node wider than block_width is one gather-add op
-//    per slope in an HBM/L2 ping-pong pass (kernel K2) per tree depth.  The
-//    root level (depth 0) is fused with the store into the reference output
-//    layout (kernel K3).
+//  * pass 0, "blocks" (kernel K1): every maximal subtree of width <=
+//    block_width.  One CTA computes a whole block for a tile of S rows,
+//    reading the input image directly in the quadrant's orientation.  A
+//    block's merge schedule depends only on its width: a per-width "shape"
+//    table of (dst, a, b, shift) ops in block-local columns (b = -1 carries
+//    a leaf one level up).  The rows a tile must load beyond S (the halo)
+//    are derived exactly from the tables by propagating the shifts
+//    backwards -- never assumed.
+//  * passes 1.. "fused upper passes" (kernel K2): the tree above the blocks,
+//    cut into bands of at most `pass_levels` levels (by height above the
+//    previous pass's output frontier).  Each band node's slopes are cut into
+//    tiles of G consecutive slopes; a tile is a small program: load the
+//    windows of the frontier columns it depends on (row window offsets and
+//    extents derived from the shifts, as for blocks), run its merge ops level
+//    by level in shared memory, store its G columns.  The last pass stores
+//    the root directly in the reference layout hough[s*W + t].
 //
-// A node at depth d writes buffer d % 2 (exactly the reference's out/tmp
-// alternation, transform.cpp:42-44), so blocks of different depths and
-// upper nodes of different depths never overwrite a value before its parent
-// reads it.
+// Pass p writes workspace buffer p % 2 and reads (p-1) % 2: every pass
+// consumes exactly the previous pass's frontier (a frontier node with no
+// work in a band is carried by a copy tile), so no value is overwritten
+// before it is read.
 #pragma once
 
 #include <cstdint>
@@ -55,7 +59,7 @@ struct BlockShape {
     int depth = 0;                 // local depth of the deepest leaf (number of steps)
     int halo = 0;                  // extra input rows a tile of S rows must load
     std::vector<int> step_offset;  // ops of step k (k = 0 is the deepest) at [step_offset[k], step_offset[k+1])
-    std::vector<Op> ops;           // r is the UNREDUCED shift t - t1; `extra` rows packed in r's high half
+    std::vector<Op> ops;           // r is the UNREDUCED shift t - t1 (< block width)
     std::vector<int> extra;        // per op: rows beyond S the op must produce
 };
 
@@ -63,9 +67,29 @@ struct BlockInst {
     int x0, shape, depth;
 };
 
-struct UpperLevel {
-    int depth;
-    std::vector<Op> ops;  // global columns, r reduced mod h
+// ---- fused upper passes (K2).  Windows: a value of column c is held for
+// rows (s0 + off + i) mod H, i in [0, S + ext).
+struct PassLoad {
+    int gcol, slot, off, ext;
+};
+struct PassOp {
+    int dst, a, b, ad, bd, ext, pad0, pad1;  // dst[i] = a[i + ad] + b[i + bd], i < S + ext (b < 0: copy)
+};
+struct PassStore {
+    int slot, gcol;
+};
+struct PassTile {
+    int load_beg, load_cnt, step_beg, nsteps, store_beg, store_cnt, nslots, max_ext;
+};
+struct FusedPass {
+    int levels = 0;  // tree levels this pass advances (max over its tiles)
+    std::vector<PassTile> tiles;
+    std::vector<PassLoad> loads;
+    std::vector<int> step_offs;  // tile steps: ops [step_offs[step_beg+k], step_offs[step_beg+k+1])
+    std::vector<PassOp> ops;
+    std::vector<PassStore> stores;
+    int max_slots = 0, max_ext = 0, tile_width = 0;
+    int64_t loaded_cells = 0;  // sum over tiles of loaded window cells at S = 0 (per-row-tile overhead)
 };
 
 // The schedule for one working orientation (width W = number of slopes,
@@ -74,13 +98,14 @@ struct SubPlan {
     int W = 0, H = 0, strategy = kTweaked, block_width = 32;
     std::vector<BlockShape> shapes;
     std::vector<BlockInst> blocks;
-    std::vector<UpperLevel> levels;  // ordered deepest first; levels.back() is the root (depth 0) if root is upper
+    std::vector<FusedPass> passes;  // after K1; passes.back() writes the root
     bool root_is_block = false;
     int max_block_width = 0;
     int max_halo = 0;
+    int tree_depth = 0;      // levels of the whole tree (= ceil(log2 W) for Tweaked)
     uint64_t additions = 0;  // count_additions_tree(W, H)
 
-    static SubPlan build(int W, int H, int strategy, int block_width);
+    static SubPlan build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width);
     std::string describe() const;
 };
 

@@ -108,12 +108,14 @@ def count_additions_tree(w: int, h: int, strategy=SplitStrategy.Tweaked) -> int:
     return int(r.value)
 
 
-def schedule(W: int, H: int, strategy=SplitStrategy.Tweaked, block_width: int = 32) -> dict:
+def schedule(W: int, H: int, strategy=SplitStrategy.Tweaked, block_width: int = 32, pass_levels: int = 4,
+             tile_width: int = 32) -> dict:
     """The host schedule tables for one orientation (no GPU needed)."""
     need = ctypes.c_size_t()
-    lib().fht_schedule_json(W, H, _strategy(strategy), block_width, None, 0, ctypes.byref(need))
+    st = _strategy(strategy)
+    lib().fht_schedule_json(W, H, st, block_width, pass_levels, tile_width, None, 0, ctypes.byref(need))
     buf = ctypes.create_string_buffer(int(need.value) + 1)
-    check(lib().fht_schedule_json(W, H, _strategy(strategy), block_width, buf, len(buf), ctypes.byref(need)))
+    check(lib().fht_schedule_json(W, H, st, block_width, pass_levels, tile_width, buf, len(buf), ctypes.byref(need)))
     return json.loads(buf.value.decode())
 
 

@@ -8,10 +8,12 @@ oracle before any CUDA runs.  Test helper only.
 import numpy as np
 
 
-def replay(cols: np.ndarray, sched: dict, S: int) -> np.ndarray:
-    """cols[x, y] = working column x, row y (W x H).  Returns OUT_0[t, s]."""
+def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None) -> np.ndarray:
+    """cols[x, y] = working column x, row y (W x H).  Returns OUT_0[t, s].
+    S = K1 row tile; pass_S = K2 row tile (default: H)."""
     W, H = cols.shape
     S = min(S, H)
+    PS = min(pass_S or H, H)
     bufs = [np.zeros((W, H), cols.dtype), np.zeros((W, H), cols.dtype)]
     for x0, shape, depth in sched["blocks"]:
         sh = sched["shapes"][shape]
@@ -29,14 +31,38 @@ def replay(cols: np.ndarray, sched: dict, S: int) -> np.ndarray:
                     nxt[dst, :n] = cur[a, :n] + cur[b, r:r + n] if b >= 0 else cur[a, :n]
                 cur = nxt
             m = min(S, H - s0)
-            bufs[depth & 1][x0:x0 + wb, s0:s0 + m] = cur[:, :m]
-    for lvl in sched["levels"]:
-        d = lvl["depth"]
-        src, dst = bufs[(d + 1) & 1], bufs[d & 1]
-        for t, a, b, r in lvl["ops"]:
-            assert 0 <= r < H
-            dst[t] = src[a] + np.roll(src[b], -r)
-    return bufs[0]
+            bufs[0][x0:x0 + wb, s0:s0 + m] = cur[:, :m]  # K1 = pass 0 -> buffer 0
+    if sched["root_is_block"]:
+        return bufs[0]
+    passes = sched["passes"]
+    result = np.zeros((W, H), cols.dtype)
+    for p, ps in enumerate(passes):
+        src = bufs[p & 1]
+        dst = result if p == len(passes) - 1 else bufs[(p + 1) & 1]
+        written = np.zeros(W, bool)
+        for lb, lc, sb, nsteps, stb, stc, nslots, max_ext in ps["tiles"]:
+            for s0 in range(0, H, PS):
+                sm = {}
+                for gcol, slot, off, ext in ps["loads"][lb:lb + lc]:
+                    sm[slot] = src[gcol][(s0 + off + np.arange(PS + ext)) % H]
+                for k in range(nsteps):
+                    step = ps["ops"][ps["step_offs"][sb + k]:ps["step_offs"][sb + k + 1]]
+                    reads = {o[1] for o in step} | {o[2] for o in step if o[2] >= 0}
+                    writes = [o[0] for o in step]
+                    assert len(set(writes)) == len(writes) and not (set(writes) & reads), "slot reuse within a step"
+                    new = {}
+                    for d, a, b, ad, bd, ext in step:
+                        n = PS + ext
+                        assert ad + n <= len(sm[a]) and (b < 0 or bd + n <= len(sm[b])), "window overrun"
+                        new[d] = sm[a][ad:ad + n] + sm[b][bd:bd + n] if b >= 0 else sm[a][ad:ad + n].copy()
+                    assert max(writes, default=-1) < nslots
+                    sm.update(new)
+                m = min(PS, H - s0)
+                for slot, gcol in ps["stores"][stb:stb + stc]:
+                    dst[gcol, s0:s0 + m] = sm[slot][:m]
+                    written[gcol] = True
+        assert written.all(), "a pass did not write every column"
+    return result
 
 
 def working_cols(img: np.ndarray, q: int) -> np.ndarray:
