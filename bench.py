@@ -197,16 +197,6 @@ def run_reference(args):
 ESZ = {"u8": 1, "i32": 4, "i64": 8, "f32": 4}
 
 
-def algorithmic_bytes(c: workloads.Config, kind: int, W: int, H: int, slots: int):
-    """per launch, each distinct input cell read once and each
-    output cell written once.  K1 (image -> pass-0 frontier): W*H*(e_in + e_acc);
-    a fused K2 pass (frontier -> next frontier / root): W*H*2*e_acc."""
-    ea = ESZ[c.acc]
-    if kind == 1:
-        return slots * W * H * (ESZ[c.dtype] + ea)
-    return slots * W * H * 2 * ea
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -268,34 +258,26 @@ def run_ours(args):
     value = sums_per_step / (ms_per_step * 1e-3) / 1e9
 
     # Per-kernel live timing (events between launches, same stream) for the roofline.
-    desc = plan.describe()
     nl = plan.launches
     ms_arr = (ctypes.c_float * nl)()
     kind_arr = (ctypes.c_int * nl)()
+    bytes_arr = (ctypes.c_double * nl)()
     got = ctypes.c_int()
     per_launch = []
     for _ in range(3):
         flush.fill_(1)
         check(lib().fht_execute_profiled(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
                                          ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
-                                         ctypes.c_void_p(stream.cuda_stream), ms_arr, kind_arr, nl, ctypes.byref(got)))
+                                         ctypes.c_void_p(stream.cuda_stream), ms_arr, kind_arr, bytes_arr, nl,
+                                         ctypes.byref(got)))
         per_launch.append(list(ms_arr)[:got.value])
     kinds = list(kind_arr)[:got.value]
+    launch_bytes = list(bytes_arr)[:got.value]
     med = [statistics.median(v) for v in zip(*per_launch)]
-    # Map each launch to its byte count.
-    g = desc["groups"][0]
-    sp = g["plan"]
-    launch_bytes = []
-    for img0 in range(0, c.batch, desc["chunk"]):
-        nimg = min(desc["chunk"], c.batch - img0)
-        slots = nimg * len(g["quadrants"])
-        launch_bytes.append(algorithmic_bytes(c, 1, sp["W"], sp["H"], slots))
-        for _ in sp["passes"]:
-            launch_bytes.append(algorithmic_bytes(c, 2, sp["W"], sp["H"], slots))
     by_kind: dict[int, list] = {}
     for kd, ms, b in zip(kinds, med, launch_bytes):
         by_kind.setdefault(kd, []).append((ms, b))
-    names = {1: "k1_blocks", 2: "k2_pass", 3: "k2_pass_root"}
+    names = {1: "k1_blocks", 4: "k1p_by32", 2: "k2_pass", 3: "k2_pass_root"}
     kernel_share = {names[kd]: sum(m for m, _ in v) for kd, v in by_kind.items()}
     dom = max(by_kind, key=lambda kd: sum(m for m, _ in by_kind[kd]))
     dom_ms = statistics.mean(m for m, _ in by_kind[dom])
@@ -308,7 +290,9 @@ def run_ours(args):
                 "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": int(dom_bytes), "avg_launch_ms": round(dom_ms, 5),
                 "step_algorithmic_bytes": int(total_bytes), "step_gbs": round(step_gbs, 1),
-                "kernel_ms": {k2: round(v, 4) for k2, v in kernel_share.items()}}
+                "kernel_ms": {k2: round(v, 4) for k2, v in kernel_share.items()},
+                "kernel_gbs": {names[kd]: round(sum(b for _, b in v) / (sum(m for m, _ in v) * 1e-3) / 1e9, 1)
+                               for kd, v in by_kind.items()}}
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:

@@ -104,12 +104,14 @@ int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void
                 int64_t out_image_stride, void* d_workspace, void* stream);
 
 /* fht_execute with a CUDA event recorded after every kernel launch on
- * `stream`; synchronises and returns each launch's duration (ms) and kind
- * (1 = K1 blocks, 2 = K2 upper level, 3 = K3 root+transpose).  For the
- * bench's live per-kernel roofline. */
+ * `stream`; synchronises and returns each launch's duration (ms), kind
+ * (1 = K1 generic blocks, 4 = K1P width-32 Brady-Yong blocks, 2 = K2 fused
+ * upper pass, 3 = K2 root pass) and algorithmic bytes (each input cell read
+ * once, each output cell written once).  For the bench's live per-kernel
+ * roofline. */
 int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
                          int64_t out_image_stride, void* d_workspace, void* stream, float* launch_ms,
-                         int* launch_kind, int max_launches, int* n_launches);
+                         int* launch_kind, double* launch_bytes, int max_launches, int* n_launches);
 
 /* Same, with HOST buffers: copies the inputs host->device, runs, copies the
  * outputs device->host and synchronises `stream`.  Uses device staging

@@ -36,7 +36,7 @@ SIGNATURES = {
     "fht_execute": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp]),
     "fht_execute_host": (_i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "fht_execute_profiled": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp, ctypes.POINTER(ctypes.c_float),
-                                  _pi, _i, _pi]),
+                                  _pi, ctypes.POINTER(ctypes.c_double), _i, _pi]),
     "fht_check_budget": (_i, [_vp, _i, _i64, _i, _pi, _vp]),
     "fht_fht2d_counted_i64": (_i, [_pi64, _i, _i, _i, _pi64, _pu64]),
     "fht_fht2d_quadrants_i64": (_i, [_pi64, _i, _i, _i, _pi64, _pi64, _pi64, _pi64, _pu64]),

@@ -81,9 +81,10 @@ bool valid_types(int in, int acc, int out) {
 struct DevTables {
     void* blob = nullptr;
     const int4* blocks = nullptr;
+    const int* by_x0 = nullptr;
     const ShapeHdr* shapes = nullptr;
     const int* step_offs = nullptr;
-    const int4* k1_ops = nullptr;
+    const fhtb::PassOpDev* k1_ops = nullptr;
     std::vector<fhtb::PassDev> passes;  // device pointers; S/L filled by create_plan
     int max_ops = 0, max_steps = 0;
 };
@@ -93,6 +94,8 @@ struct Group {
     SubPlan sp;
     DevTables dt;
     int ld = 0, S = 0, sr = 0, nbuf = 0;
+    int nblocks = 0, nby = 0;
+    bool use_by32 = false;
     size_t slot_bytes = 0;
 };
 
@@ -139,11 +142,23 @@ struct DeviceGuard {
 
 void upload(Group& g) {
     const SubPlan& sp = g.sp;
+    // Width-32 non-root blocks go to the specialised K1P kernel (4-byte
+    // accumulators); every other block to the table-driven K1.
     std::vector<int4> blocks;
-    for (const auto& b : sp.blocks) blocks.push_back(make_int4(b.x0, b.shape, b.depth, 0));
+    std::vector<int> by_x0;
+    for (const auto& b : sp.blocks) {
+        const bool by = g.use_by32 && !sp.root_is_block && sp.shapes[static_cast<size_t>(b.shape)].width == 32;
+        if (by)
+            by_x0.push_back(b.x0);
+        else
+            blocks.push_back(make_int4(b.x0, b.shape, b.depth, 0));
+    }
+    g.nblocks = static_cast<int>(blocks.size());
+    g.nby = static_cast<int>(by_x0.size());
     std::vector<ShapeHdr> shapes;
     std::vector<int> step_offs;
-    std::vector<int4> k1_ops;
+    std::vector<fhtb::PassOp> k1_ops;
+    const int mw = sp.max_block_width;
     for (const auto& s : sp.shapes) {
         ShapeHdr hdr{};
         hdr.width = s.width;
@@ -153,10 +168,21 @@ void upload(Group& g) {
         hdr.halo = s.halo;
         shapes.push_back(hdr);
         for (int o : s.step_offset) step_offs.push_back(o);
-        for (size_t k = 0; k < s.ops.size(); ++k) {
-            const auto& op = s.ops[k];
-            if (op.r < 0 || op.r > 0xffff || s.extra[k] > 0x7fff) throw FhtError(FHT_ERR_INTERNAL, "k1 op overflow");
-            k1_ops.push_back(make_int4(op.dst, op.a, op.b, op.r | (s.extra[k] << 16)));
+        // Step k (deepest first) reads buffer (nsteps-k)%2 and writes
+        // (nsteps-1-k)%2; buffer p is slots [p*mw, (p+1)*mw) of the K1 tile.
+        for (int k = 0; k < s.depth; ++k) {
+            const int ps = ((s.depth - k) & 1) * mw, pd = ((s.depth - 1 - k) & 1) * mw;
+            for (int o = s.step_offset[static_cast<size_t>(k)]; o < s.step_offset[static_cast<size_t>(k) + 1]; ++o) {
+                const auto& op = s.ops[static_cast<size_t>(o)];
+                fhtb::PassOp po{};
+                po.dst = op.dst + pd;
+                po.a = op.a + ps;
+                po.b = op.b >= 0 ? op.b + ps : -1;
+                po.ad = 0;
+                po.bd = op.r;
+                po.ext = s.extra[static_cast<size_t>(o)];
+                k1_ops.push_back(po);
+            }
         }
         g.dt.max_ops = std::max(g.dt.max_ops, static_cast<int>(s.ops.size()));
         g.dt.max_steps = std::max(g.dt.max_steps, s.depth);
@@ -170,9 +196,10 @@ void upload(Group& g) {
         return off;
     };
     const size_t o_blocks = put(blocks.data(), blocks.size() * sizeof(int4));
+    const size_t o_by = put(by_x0.data(), by_x0.size() * sizeof(int));
     const size_t o_shapes = put(shapes.data(), shapes.size() * sizeof(ShapeHdr));
     const size_t o_steps = put(step_offs.data(), step_offs.size() * sizeof(int));
-    const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(int4));
+    const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(fhtb::PassOp));
     struct PassOff {
         size_t tiles, loads, steps, ops, stores;
     };
@@ -197,9 +224,10 @@ void upload(Group& g) {
     cuda_check(cudaMemcpy(g.dt.blob, blob.data(), blob.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan tables)");
     char* base = static_cast<char*>(g.dt.blob);
     g.dt.blocks = reinterpret_cast<const int4*>(base + o_blocks);
+    g.dt.by_x0 = reinterpret_cast<const int*>(base + o_by);
     g.dt.shapes = reinterpret_cast<const ShapeHdr*>(base + o_shapes);
     g.dt.step_offs = reinterpret_cast<const int*>(base + o_steps);
-    g.dt.k1_ops = reinterpret_cast<const int4*>(base + o_k1);
+    g.dt.k1_ops = reinterpret_cast<const fhtb::PassOpDev*>(base + o_k1);
     for (size_t i = 0; i < o_passes.size(); ++i) {
         const PassOff& o = o_passes[i];
         fhtb::PassDev d{};
@@ -222,7 +250,7 @@ int env_int(const char* name, int def, int lo, int hi) {
 // Rows per K2 row tile for a pass: as many as fit `budget` bytes of shared
 // memory (max_slots slots of S + max_ext rows), capped at H; multiples of 32.
 int pass_rows(const fhtb::FusedPass& ps, int H, size_t esz, size_t budget) {
-    const long cap = static_cast<long>(budget / (esz * static_cast<size_t>(std::max(1, ps.max_slots)))) - ps.max_ext - 1;
+    const long cap = static_cast<long>(budget / (esz * static_cast<size_t>(std::max(1, ps.max_slots)))) - ps.max_ext - 20;
     if (cap >= H) return H;
     if (cap < 32) return static_cast<int>(std::max(0L, cap));
     return static_cast<int>(cap / 32 * 32);
@@ -279,11 +307,12 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         // reasonable row tile in the shared-memory budget.
         const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 100, 16, 220)) * 1024;
         const int levels = env_int("FHT_PASS_LEVELS", 4, 1, 8);
-        int tw = env_int("FHT_TILE_WIDTH", 32, 1, 4096);
+        int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
         for (;;) {
             g->sp = SubPlan::build(W, H, strategy, bw, levels, tw);
             bool ok = true;
-            for (const auto& ps : g->sp.passes) ok = ok && pass_rows(ps, H, acc_sz, budget) >= std::min(H, 32);
+            for (const auto& ps : g->sp.passes)
+                ok = ok && pass_rows(ps, H, acc_sz, budget) >= std::min(H, 32);
             if (ok) break;
             if (tw == 1) throw FhtError(FHT_ERR_INTERNAL, "fused pass does not fit shared memory");
             tw = std::max(1, tw / 2);
@@ -291,19 +320,40 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         g->qs.n = static_cast<int>(codes.size());
         for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
         g->ld = round_up(H, acc_sz == 8 ? 16 : 32);
-        int S = acc_sz == 8 ? 128 : 256;
+        // K1 rows per tile: every op's window (S + halo) fits the executor's
+        // 256-row item pair.
+        // K1 rows per tile: the fewest tiles of <= 256 rows, balanced.
+        const int smax = acc_sz == 8 ? 128 : 256;
+        const int ntile = (H + smax - 1) / smax;
+        int S = ((H + ntile - 1) / ntile + 7) & ~7;
         if (H < S) S = H;
         g->S = S;
-        g->sr = S + g->sp.max_halo;
-        if ((g->sr & 1) == 0) g->sr += 1;
+        // K1 column stride: 16-byte aligned, vector-merge slack, and room for
+        // the row-major staging tile of the horizontal loader (R x (wb+1)).
+        {
+            const int R = S + g->sp.max_halo, mw = std::max(1, g->sp.max_block_width);
+            int sr = std::max(R + 12, (R * (mw + 1) + mw - 1) / mw);
+            sr = (sr + 3) & ~3;
+            if (((sr >> 2) & 1) == 0) sr += 4;
+            g->sr = sr;
+        }
         g->nbuf = g->sp.root_is_block ? 0 : (g->sp.passes.size() > 1 ? 2 : 1);
+        g->use_by32 = acc_sz == 4 && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
         g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
         upload(*g);
         for (size_t i = 0; i < g->dt.passes.size(); ++i) {
             auto& d = g->dt.passes[i];
             d.S = pass_rows(g->sp.passes[i], H, acc_sz, budget);
-            d.L = d.S + g->sp.passes[i].max_ext;
-            if ((d.L & 1) == 0) d.L += 1;
+            {  // balance the row tiles
+                const int nt = (H + d.S - 1) / std::max(1, d.S);
+                d.S = std::min(d.S, ((H + nt - 1) / nt + 7) & ~7);
+                if (d.S > H) d.S = H;
+            }
+            // slot capacity: window + vector-merge slack, a multiple of 4 rows
+            // (16-byte aligned slots) with L/4 odd (spreads the transposed
+            // root stores over the banks)
+            d.L = (d.S + g->sp.passes[i].max_ext + 12 + 3) & ~3;
+            if (((d.L >> 2) & 1) == 0) d.L += 4;
         }
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
@@ -323,7 +373,8 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     p->ws_bytes = max_slot_bytes * static_cast<size_t>(chunk);
     const int nchunks = (batch + chunk - 1) / chunk;
     int per_chunk = 0;
-    for (auto& g : p->groups) per_chunk += 1 + static_cast<int>(g->sp.passes.size());
+    for (auto& g : p->groups)
+        per_chunk += (g->nblocks > 0 ? 1 : 0) + (g->nby > 0 ? 1 : 0) + static_cast<int>(g->sp.passes.size());
     p->launches = per_chunk * nchunks;
     return p.release();
 }
@@ -353,8 +404,10 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.ld = g.ld;
             L.acc_dtype = p->acc;
             L.S = g.S;
-            L.nblocks = static_cast<int>(g.sp.blocks.size());
+            L.nblocks = g.nblocks;
             L.blocks = g.dt.blocks;
+            L.nby = g.nby;
+            L.by_x0 = g.dt.by_x0;
             L.shapes = g.dt.shapes;
             L.step_offs = g.dt.step_offs;
             L.k1_ops = g.dt.k1_ops;
@@ -532,7 +585,7 @@ int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void
 
 int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
                          int64_t out_image_stride, void* d_workspace, void* stream, float* launch_ms, int* launch_kind,
-                         int max_launches, int* n_launches) {
+                         double* launch_bytes, int max_launches, int* n_launches) {
     struct Ctx {
         cudaStream_t st;
         std::vector<cudaEvent_t> ev;
@@ -560,6 +613,29 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
         cuda_check(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
         const int n = static_cast<int>(c.ev.size()) - 1;
         if (n_launches) *n_launches = n;
+        // Algorithmic bytes of each launch (every distinct input
+        // cell read once, every output cell written once), in launch order.
+        std::vector<double> bytes;
+        const double ein = static_cast<double>(esize(plan->in)), ea = static_cast<double>(esize(plan->acc)),
+                     eo = static_cast<double>(esize(plan->out));
+        for (int img0 = 0; img0 < plan->batch; img0 += plan->chunk) {
+            const double nimg = std::min(plan->chunk, plan->batch - img0);
+            for (auto& gp : plan->groups) {
+                const Group& g = *gp;
+                const double slots = nimg * g.qs.n, H = g.sp.H;
+                double by_cols = 0, gen_cols = 0;
+                for (const auto& b : g.sp.blocks) {
+                    const int wdt = g.sp.shapes[static_cast<size_t>(b.shape)].width;
+                    (g.use_by32 && !g.sp.root_is_block && wdt == 32 ? by_cols : gen_cols) += wdt;
+                }
+                if (g.nby > 0) bytes.push_back(slots * by_cols * H * (ein + ea));
+                if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : ea)));
+                for (size_t k = 0; k < g.sp.passes.size(); ++k)
+                    bytes.push_back(slots * g.sp.W * H * (ea + (k + 1 == g.sp.passes.size() ? eo : ea)));
+            }
+        }
+        for (int i = 0; i < n && i < max_launches && launch_bytes; ++i)
+            launch_bytes[i] = i < static_cast<int>(bytes.size()) ? bytes[static_cast<size_t>(i)] : 0.0;
         for (int i = 0; i < n && i < max_launches; ++i) {
             float ms = 0.f;
             cuda_check(cudaEventElapsedTime(&ms, c.ev[static_cast<size_t>(i)], c.ev[static_cast<size_t>(i) + 1]),

@@ -45,6 +45,59 @@ __device__ __forceinline__ In load_quadrant(const In* __restrict__ im, int q, in
     }
 }
 
+constexpr int kU = 8;  // independent global loads in flight per lane
+
+// d[i] = col[(start + i) mod H] for i in [0, n), one warp, kU loads in flight per lane.
+template <class Acc, class Src>
+__device__ __forceinline__ void warp_load_window(Acc* __restrict__ d, const Src* __restrict__ col, int start, int n,
+                                                 int H, int lane) {
+    for (int i0 = 0; i0 < n; i0 += 32 * kU) {
+        Src v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * 32 + lane;
+            if (i < n) v[u] = col[wrap_any(start + i, H)];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * 32 + lane;
+            if (i < n) d[i] = static_cast<Acc>(v[u]);
+        }
+    }
+}
+
+// Shared-memory merge of one column window: d[i] = a[i] + b[i] (b null: copy).
+template <class Acc>
+__device__ __forceinline__ void warp_merge(Acc* d, const Acc* a, const Acc* b, int n, int lane) {
+    constexpr int U = 4;
+    if (b) {
+        for (int i0 = 0; i0 < n; i0 += 32 * U) {
+            Acc x[U], y[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < n) x[u] = a[i], y[u] = b[i];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < n) d[i] = x[u] + y[u];
+            }
+        }
+    } else {
+        for (int i = lane; i < n; i += 32) d[i] = a[i];
+    }
+}
+
+// Select from the by-value parameter structs without dynamic indexing (which
+// would copy them to local memory).
+__device__ __forceinline__ int quad_code(const QuadSet& qs, int i) {
+    return i == 0 ? qs.code[0] : i == 1 ? qs.code[1] : i == 2 ? qs.code[2] : qs.code[3];
+}
+__device__ __forceinline__ void* out_ptr(const OutDesc& o, int q) {
+    return q == 0 ? o.ptr[0] : q == 1 ? o.ptr[1] : q == 2 ? o.ptr[2] : o.ptr[3];
+}
+
 template <class T>
 __device__ __forceinline__ T from_bits(int v) {
     if constexpr (std::is_same<T, float>::value) return __int_as_float(v);
@@ -56,6 +109,160 @@ __device__ __forceinline__ int to_bits(T v) {
     else return static_cast<int>(v);
 }
 
+__device__ __forceinline__ int4 lds4(const void* p) { return *reinterpret_cast<const int4*>(p); }
+__device__ __forceinline__ void sts4(void* p, int4 v) { *reinterpret_cast<int4*>(p) = v; }
+
+// 4 consecutive rows per lane, lanes contiguous (conflict-free 16-byte
+// accesses): d[i..i+4) = a[i..i+4) + bb[i+M .. i+M+4), d, a, bb 16-byte
+// aligned.  M = (shift & 3) is warp-uniform, so the selection is static.
+template <int M, class Acc>
+__device__ __forceinline__ void merge_rows4(Acc* __restrict__ d, const Acc* __restrict__ a,
+                                            const Acc* __restrict__ bb, int n, int lane) {
+    for (int i = lane * 4; i < n; i += 128) {
+        const int4 a4 = lds4(a + i);
+        const int4 b0 = lds4(bb + i);
+        const int4 b1 = M ? lds4(bb + i + 4) : b0;
+        const int bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        sts4(d + i, make_int4(to_bits<Acc>(from_bits<Acc>(a4.x) + from_bits<Acc>(bv[M + 0])),
+                              to_bits<Acc>(from_bits<Acc>(a4.y) + from_bits<Acc>(bv[M + 1])),
+                              to_bits<Acc>(from_bits<Acc>(a4.z) + from_bits<Acc>(bv[M + 2])),
+                              to_bits<Acc>(from_bits<Acc>(a4.w) + from_bits<Acc>(bv[M + 3]))));
+    }
+}
+
+// K2 window load, 4-byte types: d[i] = col[(start + i) mod H], i < n, with
+// d 16-byte aligned.  The run up to the wrap point is copied with 16-byte
+// loads/stores when `start` is 4-aligned (columns are: ld % 4 == 0); the
+// rest (after the wrap) with unrolled scalar loads.
+template <class Acc>
+__device__ __forceinline__ void warp_load_window_v(Acc* __restrict__ d, const Acc* __restrict__ col, int start,
+                                                   int n, int H, int lane) {
+    int done = 0;
+    if constexpr (sizeof(Acc) == 4) {
+        if ((start & 3) == 0) {
+            const int run = min(n, H - start) & ~3;
+            const int4* __restrict__ src = reinterpret_cast<const int4*>(col + start);
+            for (int k0 = 0; k0 < run / 4; k0 += 32 * 2) {
+                int4 v[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int k = k0 + u * 32 + lane;
+                    if (k < run / 4) v[u] = src[k];
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int k = k0 + u * 32 + lane;
+                    if (k < run / 4) sts4(d + 4 * k, v[u]);
+                }
+            }
+            done = run;
+        }
+    }
+    if (done < n) warp_load_window(d + done, col, wrap_any(start + done, H), n - done, H, lane);
+}
+
+// Shared-memory merge of one column window, d[i] = a[i] + b[bd + i] for
+// i < n (b null: copy), one warp.  4-byte types use the vector path (d, a
+// and the b slot base 16-byte aligned; rows up to bd + n + 8 are touched --
+// the slots carry that slack); int64 uses the scalar path.
+template <class Acc>
+__device__ __forceinline__ void warp_merge_any(Acc* d, const Acc* a, const Acc* b, int bd, int n, int lane) {
+    if constexpr (sizeof(Acc) == 4) {
+        if (b) {
+            const Acc* bb = b + (bd & ~3);
+            switch (bd & 3) {
+                case 0: merge_rows4<0>(d, a, bb, n, lane); break;
+                case 1: merge_rows4<1>(d, a, bb, n, lane); break;
+                case 2: merge_rows4<2>(d, a, bb, n, lane); break;
+                default: merge_rows4<3>(d, a, bb, n, lane); break;
+            }
+        } else {
+            for (int i = lane * 4; i < n; i += 128) sts4(d + i, lds4(a + i));
+        }
+    } else {
+        warp_merge(d, a, b ? b + bd : nullptr, n, lane);
+    }
+}
+
+// One op of a merge step, one warp: d[i] = a[i] + bb[i + M], i < n, for 4-byte
+// types with d, a, bb 16-byte aligned.  Lanes own 4 consecutive rows, lanes
+// contiguous (conflict-free 16-byte shared accesses); the row chunks of 128
+// are unrolled by 3 so every load of an op is issued before its adds.
+template <int M, class Acc>
+__device__ __forceinline__ void op_rows(Acc* __restrict__ d, const Acc* __restrict__ a, const Acc* __restrict__ bb,
+                                        int n, int lane) {
+    for (int i0 = lane * 4; i0 < n; i0 += 2 * 128) {
+        int4 av[2], b0[2], b1[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int i = i0 + c * 128;
+            if (i < n) {
+                av[c] = lds4(a + i);
+                b0[c] = lds4(bb + i);
+                if (M) b1[c] = lds4(bb + i + 4);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int i = i0 + c * 128;
+            if (i < n) {
+                const int bv[8] = {b0[c].x, b0[c].y, b0[c].z, b0[c].w,
+                                   M ? b1[c].x : 0, M ? b1[c].y : 0, M ? b1[c].z : 0, 0};
+                sts4(d + i, make_int4(to_bits<Acc>(from_bits<Acc>(av[c].x) + from_bits<Acc>(bv[M + 0])),
+                                      to_bits<Acc>(from_bits<Acc>(av[c].y) + from_bits<Acc>(bv[M + 1])),
+                                      to_bits<Acc>(from_bits<Acc>(av[c].z) + from_bits<Acc>(bv[M + 2])),
+                                      to_bits<Acc>(from_bits<Acc>(av[c].w) + from_bits<Acc>(bv[M + 3]))));
+            }
+        }
+    }
+}
+
+// One merge step of a tile program, all warps of the CTA, warp per op:
+//   sm[dst*stride + i] = sm[a*stride + ad + i] + sm[b*stride + bd + i],
+//   i < S + ext (b < 0: copy).
+// a and dst are 16-byte aligned (ad % 4 == 0); b is read from its aligned
+// base and the warp-uniform residue bd & 3 selects a specialised loop.
+template <class Acc, int NWARPS>
+__device__ __forceinline__ void run_step(Acc* sm, int stride, const PassOpDev* __restrict__ ops, int o_beg,
+                                         int o_end, int S, int warp, int lane) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const PassOpDev op = ops[o];
+        Acc* d = sm + (size_t)op.dst * stride;
+        const Acc* a = sm + (size_t)op.a * stride + op.ad;
+        const int n = S + op.ext;
+        if constexpr (sizeof(Acc) == 4) {
+            if (op.b < 0) {
+                for (int i = lane * 4; i < n; i += 128) sts4(d + i, lds4(a + i));
+                continue;
+            }
+            const Acc* bb = sm + (size_t)op.b * stride + (op.bd & ~3);
+            switch (op.bd & 3) {
+                case 0: op_rows<0>(d, a, bb, n, lane); break;
+                case 1: op_rows<1>(d, a, bb, n, lane); break;
+                case 2: op_rows<2>(d, a, bb, n, lane); break;
+                default: op_rows<3>(d, a, bb, n, lane); break;
+            }
+        } else {
+            warp_merge(d, a, op.b >= 0 ? sm + (size_t)op.b * stride + op.bd : nullptr, n, lane);
+        }
+    }
+}
+
+// Column store smem -> global, rows [0, n): 16-byte stores when the global
+// column start is 16-byte aligned (4-byte types), scalar tail.
+template <class Acc, class Out>
+__device__ __forceinline__ void warp_store_col(Out* __restrict__ g, const Acc* s, int n, bool aligned, int lane) {
+    int done = 0;
+    if constexpr (sizeof(Acc) == 4 && std::is_same<Acc, Out>::value) {
+        if (aligned) {
+            const int n4 = n & ~3;
+            for (int i = lane * 4; i < n4; i += 128) *reinterpret_cast<int4*>(g + i) = lds4(s + i);
+            done = n4;
+        }
+    }
+    for (int i = done + lane; i < n; i += 32) g[i] = static_cast<Out>(s[i]);
+}
+
 __device__ __forceinline__ size_t k1_ops_offset_dev(size_t esz, int max_width, int sr) {
     return (2 * static_cast<size_t>(max_width) * sr * esz + 15) / 16 * 16;
 }
@@ -63,16 +270,14 @@ __device__ __forceinline__ size_t k1_ops_offset_dev(size_t esz, int max_width, i
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
 template <class In, class Acc, class Out>
-__global__ void __launch_bounds__(kThreads) k1_blocks(
+__global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const In* __restrict__ img, int img_w, int img_h, long long img_stride, int img0, QuadSet qs, int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
-    const int* __restrict__ step_offs, const int4* __restrict__ ops, int max_width, int sr, int max_ops,
+    const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, int max_width, int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);
-    Acc* buf1 = buf0 + (size_t)max_width * sr;
-    int4* sops = reinterpret_cast<int4*>(smem_raw + k1_ops_offset_dev(sizeof(Acc), max_width, sr));
-    int* soffs = reinterpret_cast<int*>(sops + max_ops);
+    Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
+    Acc* buf1 = buf0 + (size_t)max_width * sr;     // slots [max_width, 2 max_width): parity 1
 
     const int tid = threadIdx.x;
     const int4 blk = blocks[blockIdx.y];
@@ -80,54 +285,66 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
     const ShapeHdr hdr = shapes[blk.y];
     const int wb = hdr.width, nsteps = hdr.nsteps;
     const int R = S + hdr.halo;
-    const int nops_total = wb * nsteps;
-    for (int k = tid; k < nops_total; k += kThreads) sops[k] = ops[hdr.op_base + k];
-    for (int k = tid; k <= nsteps; k += kThreads) soffs[k] = step_offs[hdr.step_base + k];
 
     const int slot = blockIdx.z;
     const int nq = qs.n;
     const int img_i = img0 + slot / nq;
-    const int q = qs.code[slot % nq];
+    const int q = quad_code(qs, slot % nq);
     const In* __restrict__ im = img + (size_t)img_i * img_stride;
     const int s0 = blockIdx.x * S;
 
     // Load the tile: values of depth `nsteps` (the leaves) into buf[nsteps & 1].
     Acc* lbuf = (nsteps & 1) ? buf1 : buf0;
-    const int cells = wb * R;
-    if (q < 2) {  // working column = image column: contiguous along c
-        for (int k = tid; k < cells; k += kThreads) {
-            const int c = k % wb, i = k / wb;
-            const int y = wrap_any(s0 + i, H);
-            lbuf[c * sr + i] = static_cast<Acc>(load_quadrant(im, q, x0 + c, y, img_w, img_h));
+    const int warp = tid >> 5, lane = tid & 31;
+    constexpr int kWarps = kThreads / 32;
+    if (q < 2) {
+        // working column = image column (flipped for horiz_neg): a tile row is
+        // wb contiguous image pixels.  Stage row-major (row stride wb+1, so
+        // both the row writes and the column reads below are bank-conflict
+        // free) in the buffer that does not receive the leaves, then
+        // transpose into the column-major leaf buffer.
+        Acc* stage = (nsteps & 1) ? buf0 : buf1;
+        const int sw = wb + 1;
+        const int xa = (q == 1) ? img_w - 1 - x0 : x0;  // image x of working column 0
+        const int dx = (q == 1) ? -1 : 1;
+        constexpr int kUH = 8;
+        for (int ib = warp; ib < R; ib += kWarps * kUH) {
+            In v[kUH][2];
+#pragma unroll
+            for (int u = 0; u < kUH; ++u) {
+                const int i = ib + u * kWarps;
+                if (i < R) {
+                    const In* __restrict__ rowp = im + (size_t)wrap_any(s0 + i, H) * img_w;
+                    if (lane < wb) v[u][0] = rowp[xa + dx * lane];
+                    if (lane + 32 < wb) v[u][1] = rowp[xa + dx * (lane + 32)];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUH; ++u) {
+                const int i = ib + u * kWarps;
+                if (i < R) {
+                    if (lane < wb) stage[i * sw + lane] = static_cast<Acc>(v[u][0]);
+                    if (lane + 32 < wb) stage[i * sw + lane + 32] = static_cast<Acc>(v[u][1]);
+                }
+            }
         }
-    } else {  // working column = image row: contiguous along i
-        for (int k = tid; k < cells; k += kThreads) {
-            const int i = k % R, c = k / R;
-            const int y = wrap_any(s0 + i, H);
-            lbuf[c * sr + i] = static_cast<Acc>(load_quadrant(im, q, x0 + c, y, img_w, img_h));
+        __syncthreads();
+        for (int c = warp; c < wb; c += kWarps)
+            for (int i = lane; i < R; i += 32) lbuf[c * sr + i] = stage[i * sw + c];
+    } else {
+        // working column = image row (reversed rows for vert_neg): contiguous.
+        for (int c = warp; c < wb; c += kWarps) {
+            const int row = (q == 2) ? x0 + c : img_h - 1 - (x0 + c);
+            warp_load_window(lbuf + c * sr, im + (size_t)row * img_w, s0, R, H, lane);
         }
     }
 
-    // Merge steps, deepest first: step k writes local depth nsteps-1-k.
-    const int warp = tid >> 5, lane = tid & 31;
+    // Merge steps, deepest first: step k writes local depth nsteps-1-k into
+    // the buffer of that parity (ops carry parity-offset slot numbers).
     for (int k = 0; k < nsteps; ++k) {
         __syncthreads();
-        const Acc* src = ((nsteps - k) & 1) ? buf1 : buf0;
-        Acc* dst = ((nsteps - 1 - k) & 1) ? buf1 : buf0;
-        const int o_beg = soffs[k], o_end = soffs[k + 1];
-        for (int o = o_beg + warp; o < o_end; o += kThreads / 32) {
-            const int4 op = sops[o];
-            const int r = op.w & 0xffff;
-            const int rows = S + (op.w >> 16);
-            const Acc* a = src + op.y * sr;
-            Acc* d = dst + op.x * sr;
-            if (op.z >= 0) {
-                const Acc* b = src + op.z * sr + r;
-                for (int i = lane; i < rows; i += 32) d[i] = a[i] + b[i];
-            } else {
-                for (int i = lane; i < rows; i += 32) d[i] = a[i];
-            }
-        }
+        run_step<Acc, kWarps>(buf0, sr, ops + hdr.op_base, step_offs[hdr.step_base + k],
+                              step_offs[hdr.step_base + k + 1], S, warp, lane);
     }
     __syncthreads();
 
@@ -135,27 +352,178 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
     const int rows_out = min(S, H - s0);
     if (!root_is_block) {
         Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;  // pass 0 output: buffer 0
-        const int n = wb * rows_out;
-        for (int k = tid; k < n; k += kThreads) {
-            const int i = k % rows_out, c = k / rows_out;
-            dstw[(size_t)(x0 + c) * ld + s0 + i] = buf0[c * sr + i];
-        }
+        const bool al = ((ld | s0) & 3) == 0;
+        for (int c = warp; c < wb; c += kWarps)
+            warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, buf0 + c * sr, rows_out, al, lane);
     } else {
-        Out* o = reinterpret_cast<Out*>(out.ptr[q]) + (size_t)img_i * out.img_stride;
-        const int n = wb * rows_out;
-        if (out.layout == 0) {
-            for (int k = tid; k < n; k += kThreads) {
-                const int c = k % wb, i = k / wb;
-                o[(size_t)(s0 + i) * W + c] = static_cast<Out>(buf0[c * sr + i]);
-            }
+        Out* o = reinterpret_cast<Out*>(out_ptr(out, q)) + (size_t)img_i * out.img_stride;
+        if (out.layout == 0) {  // rows of wb contiguous slopes
+            for (int i = warp; i < rows_out; i += kWarps)
+                for (int c = lane; c < wb; c += 32) o[(size_t)(s0 + i) * W + c] = static_cast<Out>(buf0[c * sr + i]);
         } else {
-            for (int k = tid; k < n; k += kThreads) {
-                const int i = k % rows_out, c = k / rows_out;
-                o[(size_t)c * H + s0 + i] = static_cast<Out>(buf0[c * sr + i]);
-            }
+            for (int c = warp; c < wb; c += kWarps)
+                for (int i = lane; i < rows_out; i += 32) o[(size_t)c * H + s0 + i] = static_cast<Out>(buf0[c * sr + i]);
         }
     }
 }
+
+// ------------------------------------------------------------------ K1P
+// Specialised pass 0 for the common block: a width-32 Brady-Yong subtree
+// (every power-of-two block; all but at most one block of a Tweaked tree).
+// Its 5 levels' (t0, t1, shift) are compile-time constants (BYOp), so the
+// shared-memory addresses are immediate offsets and each shift's residue
+// mod 4 is static.  512 threads; warp w owns columns w and w + 16 at every
+// level; lanes own 4 consecutive rows (16-byte shared accesses, lanes
+// contiguous: conflict-free).  Leaves live in slots [32, 64), level L
+// writes parity (5 - L) & 1, the block root ends in slots [0, 32).
+constexpr int kBYW = 32;        // block width
+constexpr int kBYMaxS = 256;    // rows per tile (host guarantees S <= 256)
+constexpr int kBYSR = 300;      // slot stride: >= 256 + 31 + 12, multiple of 4, /4 odd
+constexpr int kThreadsBY = 512;
+constexpr int kWarpsBY = kThreadsBY / 32;
+
+__host__ __device__ constexpr int rhu_c(int num, int den) { return (2 * num + den) / (2 * den); }
+
+template <int L, int T>
+struct BYOp {  // level L in 1..5 merges widths 2^(L-1) -> 2^L; T = block-local column
+    static constexpr int w = 1 << L, w0 = w >> 1, x0 = (T / w) * w, tl = T % w;
+    static constexpr int t0 = rhu_c(tl * (w0 - 1), w - 1);  // = t1 (both halves have width w0)
+    static constexpr int a = x0 + t0, b = x0 + w0 + t0, r = tl - t0;
+    static constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
+};
+
+template <class Acc, int L, int T>
+__device__ __forceinline__ void by_op(Acc* sm, int S, int lane) {
+    using O = BYOp<L, T>;
+    constexpr int M = O::r & 3;
+    const int n = S + kBYW - (1 << L);  // rows this level must produce (remaining halo)
+    Acc* d = sm + (O::dst + T) * kBYSR + lane * 4;
+    const Acc* a = sm + (O::src + O::a) * kBYSR + lane * 4;
+    const Acc* bb = sm + (O::src + O::b) * kBYSR + (O::r & ~3) + lane * 4;
+    int4 av[3], b0[3], b1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (lane * 4 + 128 * c < n) {
+            av[c] = lds4(a + 128 * c);
+            b0[c] = lds4(bb + 128 * c);
+            if (M) b1[c] = lds4(bb + 128 * c + 4);
+        }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        if (lane * 4 + 128 * c < n) {
+            const int bv[8] = {b0[c].x, b0[c].y, b0[c].z, b0[c].w,
+                               M ? b1[c].x : 0, M ? b1[c].y : 0, M ? b1[c].z : 0, 0};
+            sts4(d + 128 * c, make_int4(to_bits<Acc>(from_bits<Acc>(av[c].x) + from_bits<Acc>(bv[M + 0])),
+                                        to_bits<Acc>(from_bits<Acc>(av[c].y) + from_bits<Acc>(bv[M + 1])),
+                                        to_bits<Acc>(from_bits<Acc>(av[c].z) + from_bits<Acc>(bv[M + 2])),
+                                        to_bits<Acc>(from_bits<Acc>(av[c].w) + from_bits<Acc>(bv[M + 3]))));
+        }
+}
+
+template <class Acc, int L, int W = 0>
+__device__ __forceinline__ void by_level(Acc* sm, int S, int warp, int lane) {
+    if constexpr (W < kWarpsBY) {
+        if (warp == W) {
+            by_op<Acc, L, W>(sm, S, lane);
+            by_op<Acc, L, W + kWarpsBY>(sm, S, lane);
+        } else {
+            by_level<Acc, L, W + 1>(sm, S, warp, lane);
+        }
+    }
+}
+
+// grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
+template <class In, class Acc>
+__global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
+                                                          long long img_stride, int img0, QuadSet qs, int W, int H,
+                                                          int ld, int S, const int* __restrict__ bx0,
+                                                          Acc* __restrict__ ws, int nbuf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Acc* sm = reinterpret_cast<Acc*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int x0 = bx0[blockIdx.y];
+    const int slot = blockIdx.z;
+    const int nq = qs.n;
+    const int img_i = img0 + slot / nq;
+    const int q = quad_code(qs, slot % nq);
+    const In* __restrict__ im = img + (size_t)img_i * img_stride;
+    const int s0 = blockIdx.x * S;
+    const int R = S + kBYW - 1;
+    Acc* leaves = sm + kBYW * kBYSR;  // parity 1
+    constexpr int kRowsPerLane = (kBYMaxS + kBYW - 1 + 31) / 32;  // 9
+    if (q < 2) {
+        // image rows: 32 contiguous pixels per tile row; stage row-major
+        // (stride 33, conflict-free both ways) in parity 0, then transpose.
+        Acc* stage = sm;
+        const int xx = (q == 1) ? img_w - 1 - (x0 + lane) : x0 + lane;
+        constexpr int kRowsPerWarp = (kBYMaxS + kBYW - 1 + kWarpsBY - 1) / kWarpsBY;  // 18
+        In v[kRowsPerWarp];
+#pragma unroll
+        for (int k = 0; k < kRowsPerWarp; ++k) {
+            const int i = warp + k * kWarpsBY;
+            if (i < R) v[k] = im[(size_t)wrap_any(s0 + i, H) * img_w + xx];
+        }
+#pragma unroll
+        for (int k = 0; k < kRowsPerWarp; ++k) {
+            const int i = warp + k * kWarpsBY;
+            if (i < R) stage[i * 33 + lane] = static_cast<Acc>(v[k]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = warp + h * kWarpsBY;
+#pragma unroll
+            for (int k = 0; k < kRowsPerLane; ++k) {
+                const int i = lane + 32 * k;
+                if (i < R) leaves[c * kBYSR + i] = stage[i * 33 + c];
+            }
+        }
+    } else {
+        // image rows are working columns: contiguous windows, 18 loads in flight per lane
+        In v[2][kRowsPerLane];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = warp + h * kWarpsBY;
+            const int row = (q == 2) ? x0 + c : img_h - 1 - (x0 + c);
+            const In* __restrict__ rp = im + (size_t)row * img_w;
+#pragma unroll
+            for (int k = 0; k < kRowsPerLane; ++k) {
+                const int i = lane + 32 * k;
+                if (i < R) v[h][k] = rp[wrap_any(s0 + i, H)];
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = warp + h * kWarpsBY;
+#pragma unroll
+            for (int k = 0; k < kRowsPerLane; ++k) {
+                const int i = lane + 32 * k;
+                if (i < R) leaves[c * kBYSR + i] = static_cast<Acc>(v[h][k]);
+            }
+        }
+    }
+    __syncthreads();
+    by_level<Acc, 1>(sm, S, warp, lane);
+    __syncthreads();
+    by_level<Acc, 2>(sm, S, warp, lane);
+    __syncthreads();
+    by_level<Acc, 3>(sm, S, warp, lane);
+    __syncthreads();
+    by_level<Acc, 4>(sm, S, warp, lane);
+    __syncthreads();
+    by_level<Acc, 5>(sm, S, warp, lane);
+    __syncthreads();
+    const int rows_out = min(S, H - s0);
+    Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
+    const bool al = ((ld | s0) & 3) == 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = warp + h * kWarpsBY;
+        warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, sm + c * kBYSR, rows_out, al, lane);
+    }
+}
+
+size_t k1_by32_smem_bytes() { return (2 * kBYW * kBYSR + 16) * 4; }
 
 // ------------------------------------------------------------------- K2
 // One fused upper pass.  grid: x = row tile (S rows), y = tile (G slopes of
@@ -165,14 +533,16 @@ __global__ void __launch_bounds__(kThreads) k1_blocks(
 // major, row capacity L), then store its G columns -- into the other
 // workspace buffer, or (root pass) straight into the output in the
 // reference layout hough[s*W + t] (transform.cpp:80-83).
+constexpr int kThreads2 = 512;
+
 template <class Acc, class Out>
-__global__ void __launch_bounds__(kThreads) k2_pass(PassDev ps, const Acc* __restrict__ src,
+__global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int kWarps = kThreads / 32;
+    constexpr int kWarps = kThreads2 / 32;
     const PassTileDev tile = ps.tiles[blockIdx.y];
     const int S = ps.S, L = ps.L;
     const int s0 = blockIdx.x * S;
@@ -182,56 +552,58 @@ __global__ void __launch_bounds__(kThreads) k2_pass(PassDev ps, const Acc* __res
     // 1. windows of the input columns
     for (int l = warp; l < tile.load_cnt; l += kWarps) {
         const int4 ld4 = ps.loads[tile.load_beg + l];
-        const Acc* __restrict__ col = in + (size_t)ld4.x * ld;
-        Acc* __restrict__ d = sm + (size_t)ld4.y * L;
-        const int n = S + ld4.w;
-        int y = wrap_any(s0 + ld4.z + lane, H);
-        for (int i = lane; i < n; i += 32) {
-            d[i] = col[y];
-            y += 32;
-            if (y >= H) y = wrap_any(y, H);
-        }
+        warp_load_window_v(sm + (size_t)ld4.y * L, in + (size_t)ld4.x * ld, wrap_any(s0 + ld4.z, H), S + ld4.w, H,
+                           lane);
     }
     // 2. merge levels
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
-        const int o_beg = ps.step_offs[tile.step_beg + k], o_end = ps.step_offs[tile.step_beg + k + 1];
-        for (int o = o_beg + warp; o < o_end; o += kWarps) {
-            const PassOpDev op = ps.ops[o];
-            const Acc* a = sm + (size_t)op.a * L + op.ad;
-            Acc* d = sm + (size_t)op.dst * L;
-            const int n = S + op.ext;
-            if (op.b >= 0) {
-                const Acc* b = sm + (size_t)op.b * L + op.bd;
-                for (int i = lane; i < n; i += 32) d[i] = a[i] + b[i];
-            } else {
-                for (int i = lane; i < n; i += 32) d[i] = a[i];
-            }
-        }
+        run_step<Acc, kWarps>(sm, L, ps.ops, ps.step_offs[tile.step_beg + k], ps.step_offs[tile.step_beg + k + 1], S,
+                              warp, lane);
     }
     __syncthreads();
     // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)
     const int rows = min(S, H - s0);
     if (!final_pass) {
         Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
+        const bool al = ((ld | s0) & 3) == 0;
         for (int c = warp; c < tile.store_cnt; c += kWarps) {
             const int2 st = ps.stores[tile.store_beg + c];
-            const Acc* sv = sm + (size_t)st.x * L;
-            Acc* __restrict__ dcol = o + (size_t)st.y * ld + s0;
-            for (int i = lane; i < rows; i += 32) dcol[i] = sv[i];
+            warp_store_col<Acc, Acc>(o + (size_t)st.y * ld + s0, sm + (size_t)st.x * L, rows, al, lane);
         }
     } else {
         const int nq = qs.n;
         Out* __restrict__ o =
-            reinterpret_cast<Out*>(out.ptr[qs.code[slot % nq]]) + (size_t)(img0 + slot / nq) * out.img_stride;
+            reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, slot % nq))) + (size_t)(img0 + slot / nq) * out.img_stride;
         const int nc = tile.store_cnt;
         if (out.layout == 0) {
-            // stores of a tile are consecutive slopes: write rows of nc contiguous t
+            // the stores of a tile are consecutive slopes: each warp writes rows
+            // of nc (<= 64) contiguous t
             const int t0 = ps.stores[tile.store_beg].y;
-            for (int k = tid; k < nc * rows; k += kThreads) {
-                const int c = k % nc, i = k / nc;
-                const int2 st = ps.stores[tile.store_beg + c];
-                o[(size_t)(s0 + i) * W + t0 + c] = static_cast<Out>(sm[(size_t)st.x * L + i]);
+            const int sl0 = lane < nc ? ps.stores[tile.store_beg + lane].x : 0;
+            const int sl1 = lane + 32 < nc ? ps.stores[tile.store_beg + lane + 32].x : 0;
+            if constexpr (sizeof(Acc) == 4) {
+                // lane = slope; 16-byte smem reads of 4 rows, 4 coalesced row stores
+                for (int i = warp * 4; i < rows; i += kWarps * 4) {
+                    Out* __restrict__ orow = o + (size_t)(s0 + i) * W + t0;
+                    const int nr = min(4, rows - i);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        if (c >= nc) continue;
+                        const int4 v4 = lds4(sm + (size_t)(h ? sl1 : sl0) * L + i);
+                        const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k < nr) orow[(size_t)k * W + c] = static_cast<Out>(from_bits<Acc>(vv[k]));
+                    }
+                }
+            } else {
+                for (int i = warp; i < rows; i += kWarps) {
+                    Out* __restrict__ orow = o + (size_t)(s0 + i) * W + t0;
+                    if (lane < nc) orow[lane] = static_cast<Out>(sm[(size_t)sl0 * L + i]);
+                    if (lane + 32 < nc) orow[lane + 32] = static_cast<Out>(sm[(size_t)sl1 * L + i]);
+                }
             }
         } else {
             for (int c = warp; c < nc; c += kWarps) {
@@ -269,12 +641,26 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     auto k1 = k1_blocks<In, Acc, Out>;
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
-    dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
-    k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride, g.img0, g.qs,
-                                   g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs, g.k1_ops, g.k1_max_width,
-                                   g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out);
-    ++launches;
-    if (hook) hook(ctx, 1);
+    if constexpr (sizeof(Acc) == 4) {
+        if (g.nby > 0) {
+            auto kb = k1_by32<In, Acc>;
+            const int sm_by = static_cast<int>(k1_by32_smem_bytes());
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
+            dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
+            kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride,
+                                              g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
+            ++launches;
+            if (hook) hook(ctx, 4);
+        }
+    }
+    if (g.nblocks > 0) {
+        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
+        k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride, g.img0,
+                                       g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs, g.k1_ops,
+                                       g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out);
+        ++launches;
+        if (hook) hook(ctx, 1);
+    }
     if (g.root_is_block) return launches;
     const long long slot_elems = (long long)g.nbuf * g.W * g.ld;
     for (int p = 0; p < g.npasses; ++p) {
@@ -286,7 +672,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         auto k2 = k2_pass<Acc, Out>;
         cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
-        k2<<<g2, kThreads, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
+        k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
         ++launches;
         if (hook) hook(ctx, final_pass ? 3 : 2);
     }
@@ -301,13 +687,14 @@ static size_t k1_ops_offset(int acc_dtype, int max_width, int sr) {
 }
 
 size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps) {
-    return k1_ops_offset(acc_dtype, max_width, sr) + static_cast<size_t>(max_ops) * sizeof(int4) +
-           static_cast<size_t>(max_steps + 1) * sizeof(int) + 16;
+    (void)max_ops;
+    (void)max_steps;
+    return k1_ops_offset(acc_dtype, max_width, sr) + 64;  // two slot buffers + vector-read slack
 }
 
 size_t k2_smem_bytes(int acc_dtype, int max_slots, int L) {
     const size_t esz = acc_dtype == kI64 ? 8 : 4;
-    return static_cast<size_t>(max_slots) * L * esz;
+    return (static_cast<size_t>(max_slots) * L + 16) * esz;  // +16: vector-merge read slack
 }
 
 int launch_group(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* ctx) {

@@ -68,11 +68,13 @@ struct GroupLaunch {
     int acc_dtype;
     // K1
     int S;
-    int nblocks;
+    int nblocks;        // generic (table-driven) blocks
     const int4* blocks;
+    int nby;            // width-32 Brady-Yong blocks for the specialised K1P (4-byte accumulators)
+    const int* by_x0;
     const ShapeHdr* shapes;
     const int* step_offs;
-    const int4* k1_ops;
+    const PassOpDev* k1_ops;  // per-shape ops, slots pre-offset by buffer parity
     int k1_max_ops, k1_max_steps, k1_max_width, k1_sr;
     bool root_is_block;
     // fused upper passes (K2), in execution order; the last writes the root
@@ -88,8 +90,9 @@ size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_
 size_t k2_smem_bytes(int acc_dtype, int max_slots, int L);
 // Launch every kernel of one orientation group / chunk on `stream`.
 // Returns the number of kernel launches, or -1 on an unsupported type combination.
-// `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1, 2 = K2
-// (fused upper pass), 3 = K2 writing the root.
+// `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1 (generic
+// blocks), 4 = K1P (width-32 Brady-Yong blocks), 2 = K2 (fused upper pass),
+// 3 = K2 writing the root.
 typedef void (*LaunchHook)(void* ctx, int kind);
 int launch_group(const GroupLaunch& g, cudaStream_t stream, LaunchHook hook = nullptr, void* ctx = nullptr);
 

@@ -148,6 +148,11 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
     }
     for (size_t qi = 0; qi < order.size(); ++qi) {
         const int n = order[qi];
+        // All consumers of n are known now: align its window starts down to a
+        // multiple of 4 rows, so every a-operand and destination of the
+        // kernel's 16-byte vector merges is aligned (only b is shifted).
+        for (Entry& e : ent[static_cast<size_t>(n)])
+            if (e.seen) e.lo &= ~3;
         if (front[static_cast<size_t>(n)]) continue;  // input node
         const Node& nd = nodes[static_cast<size_t>(n)];
         const int c0 = nd.child[0], c1 = nd.child[1];
