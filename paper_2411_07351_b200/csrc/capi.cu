@@ -238,6 +238,10 @@ void upload(Group& g) {
         d.stores = reinterpret_cast<const int2*>(base + o.stores);
         d.ntiles = static_cast<int>(sp.passes[i].tiles.size());
         d.max_slots = sp.passes[i].max_slots;
+        d.max_tile_ops = 0;
+        for (const auto& t : sp.passes[i].tiles)
+            d.max_tile_ops = std::max(d.max_tile_ops, sp.passes[i].step_offs[static_cast<size_t>(t.step_beg + t.nsteps)] -
+                                                          sp.passes[i].step_offs[static_cast<size_t>(t.step_beg)]);
         g.dt.passes.push_back(d);
     }
 }
@@ -408,6 +412,8 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.blocks = g.dt.blocks;
             L.nby = g.nby;
             L.by_x0 = g.dt.by_x0;
+            L.k1p_variant = env_int("FHT_K1P_VARIANT", 0, 0, 1);
+            L.k2_variant = env_int("FHT_K2_VARIANT", 1, 0, 1);
             L.shapes = g.dt.shapes;
             L.step_offs = g.dt.step_offs;
             L.k1_ops = g.dt.k1_ops;

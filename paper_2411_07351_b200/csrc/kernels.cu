@@ -112,6 +112,113 @@ __device__ __forceinline__ int to_bits(T v) {
 __device__ __forceinline__ int4 lds4(const void* p) { return *reinterpret_cast<const int4*>(p); }
 __device__ __forceinline__ void sts4(void* p, int4 v) { *reinterpret_cast<int4*>(p) = v; }
 
+// 32-bit shared-window addressing for the merge inner loops (keeps the
+// compiler from rematerialising the shared window base per access).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ int4 lds4u(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts4u(uint32_t a, int4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// d[k] = a[k] + b[k + M] for one lane's 4 rows; b0/b1 are the aligned b
+// vectors at and after the lane's rows.
+template <int M, class Acc>
+__device__ __forceinline__ int4 add_shift(int4 av, int4 b0, int4 b1) {
+    const int bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    return make_int4(to_bits<Acc>(from_bits<Acc>(av.x) + from_bits<Acc>(bv[M + 0])),
+                     to_bits<Acc>(from_bits<Acc>(av.y) + from_bits<Acc>(bv[M + 1])),
+                     to_bits<Acc>(from_bits<Acc>(av.z) + from_bits<Acc>(bv[M + 2])),
+                     to_bits<Acc>(from_bits<Acc>(av.w) + from_bits<Acc>(bv[M + 3])));
+}
+
+// One op, one warp, 4-byte types: rows [0, n) of d = a + (b shifted by M),
+// byte addresses in the shared window (d, a, bb 16-byte aligned, bb the
+// aligned base of the shifted b).  Lanes own 4 consecutive rows, lanes
+// contiguous (conflict-free); warp-uniform full 128-row chunks two at a time
+// (all loads before the adds), then one predicated tail chunk.
+template <int M, class Acc>
+__device__ __forceinline__ void rows_op(uint32_t d, uint32_t a, uint32_t bb, int n, int lane) {
+    const int nfull = n >> 7;
+    uint32_t off = lane * 16u;
+    int c = 0;
+    for (; c + 2 <= nfull; c += 2, off += 1024u) {
+        const int4 a0 = lds4u(a + off), a1 = lds4u(a + off + 512u);
+        const int4 p0 = lds4u(bb + off), p1 = lds4u(bb + off + 512u);
+        int4 q0 = p0, q1 = p1;
+        if (M) {
+            q0 = lds4u(bb + off + 16u);
+            q1 = lds4u(bb + off + 528u);
+        }
+        sts4u(d + off, add_shift<M, Acc>(a0, p0, q0));
+        sts4u(d + off + 512u, add_shift<M, Acc>(a1, p1, q1));
+    }
+    if (c < nfull) {
+        const int4 a0 = lds4u(a + off), p0 = lds4u(bb + off);
+        const int4 q0 = M ? lds4u(bb + off + 16u) : p0;
+        sts4u(d + off, add_shift<M, Acc>(a0, p0, q0));
+        off += 512u;
+    }
+    if (lane * 4 < n - (nfull << 7)) {
+        const int4 a0 = lds4u(a + off), p0 = lds4u(bb + off);
+        const int4 q0 = M ? lds4u(bb + off + 16u) : p0;
+        sts4u(d + off, add_shift<M, Acc>(a0, p0, q0));
+    }
+}
+
+// Same op with int4 indices into the shared array (the compiler keeps one
+// shared base and schedules the loads freely): rows [0, n) of
+// V[d4..] = V[a4..] + (V[b4..] shifted by M).  Three predicated 128-row
+// chunks per iteration, every load of an iteration before its stores.
+template <int M, class Acc>
+__device__ __forceinline__ void rows_v(int4* __restrict__ V, int d4, int a4, int b4, int n, int lane) {
+    for (int i0 = lane; i0 * 4 < n; i0 += 96) {
+        int4 av[3], b0[3], b1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int k = i0 + 32 * c;
+            if (k * 4 < n) {
+                av[c] = V[a4 + k];
+                b0[c] = V[b4 + k];
+                if (M) b1[c] = V[b4 + k + 1];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int k = i0 + 32 * c;
+            if (k * 4 < n) V[d4 + k] = add_shift<M, Acc>(av[c], b0[c], M ? b1[c] : b0[c]);
+        }
+    }
+}
+
+template <class Acc>
+__device__ __forceinline__ void rows_v_any(int4* V, int d4, int a4, int b4, int bd, int n, int lane) {
+    b4 += bd >> 2;
+    switch (bd & 3) {
+        case 0: rows_v<0, Acc>(V, d4, a4, b4, n, lane); break;
+        case 1: rows_v<1, Acc>(V, d4, a4, b4, n, lane); break;
+        case 2: rows_v<2, Acc>(V, d4, a4, b4, n, lane); break;
+        default: rows_v<3, Acc>(V, d4, a4, b4, n, lane); break;
+    }
+}
+
+template <class Acc>
+__device__ __forceinline__ void rows_op_any(uint32_t d, uint32_t a, uint32_t b, int bd, int n, int lane) {
+    const uint32_t bb = b + static_cast<uint32_t>(bd & ~3) * 4u;
+    switch (bd & 3) {
+        case 0: rows_op<0, Acc>(d, a, bb, n, lane); break;
+        case 1: rows_op<1, Acc>(d, a, bb, n, lane); break;
+        case 2: rows_op<2, Acc>(d, a, bb, n, lane); break;
+        default: rows_op<3, Acc>(d, a, bb, n, lane); break;
+    }
+}
+
 // 4 consecutive rows per lane, lanes contiguous (conflict-free 16-byte
 // accesses): d[i..i+4) = a[i..i+4) + bb[i+M .. i+M+4), d, a, bb 16-byte
 // aligned.  M = (shift & 3) is warp-uniform, so the selection is static.
@@ -184,66 +291,45 @@ __device__ __forceinline__ void warp_merge_any(Acc* d, const Acc* a, const Acc* 
     }
 }
 
-// One op of a merge step, one warp: d[i] = a[i] + bb[i + M], i < n, for 4-byte
-// types with d, a, bb 16-byte aligned.  Lanes own 4 consecutive rows, lanes
-// contiguous (conflict-free 16-byte shared accesses); the row chunks of 128
-// are unrolled by 3 so every load of an op is issued before its adds.
-template <int M, class Acc>
-__device__ __forceinline__ void op_rows(Acc* __restrict__ d, const Acc* __restrict__ a, const Acc* __restrict__ bb,
-                                        int n, int lane) {
-    for (int i0 = lane * 4; i0 < n; i0 += 2 * 128) {
-        int4 av[2], b0[2], b1[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int i = i0 + c * 128;
-            if (i < n) {
-                av[c] = lds4(a + i);
-                b0[c] = lds4(bb + i);
-                if (M) b1[c] = lds4(bb + i + 4);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int i = i0 + c * 128;
-            if (i < n) {
-                const int bv[8] = {b0[c].x, b0[c].y, b0[c].z, b0[c].w,
-                                   M ? b1[c].x : 0, M ? b1[c].y : 0, M ? b1[c].z : 0, 0};
-                sts4(d + i, make_int4(to_bits<Acc>(from_bits<Acc>(av[c].x) + from_bits<Acc>(bv[M + 0])),
-                                      to_bits<Acc>(from_bits<Acc>(av[c].y) + from_bits<Acc>(bv[M + 1])),
-                                      to_bits<Acc>(from_bits<Acc>(av[c].z) + from_bits<Acc>(bv[M + 2])),
-                                      to_bits<Acc>(from_bits<Acc>(av[c].w) + from_bits<Acc>(bv[M + 3]))));
-            }
-        }
-    }
-}
-
 // One merge step of a tile program, all warps of the CTA, warp per op:
 //   sm[dst*stride + i] = sm[a*stride + ad + i] + sm[b*stride + bd + i],
 //   i < S + ext (b < 0: copy).
 // a and dst are 16-byte aligned (ad % 4 == 0); b is read from its aligned
 // base and the warp-uniform residue bd & 3 selects a specialised loop.
-template <class Acc, int NWARPS>
+template <class Acc, int NWARPS, int V = 1>
 __device__ __forceinline__ void run_step(Acc* sm, int stride, const PassOpDev* __restrict__ ops, int o_beg,
                                          int o_end, int S, int warp, int lane) {
-    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
-        const PassOpDev op = ops[o];
-        Acc* d = sm + (size_t)op.dst * stride;
-        const Acc* a = sm + (size_t)op.a * stride + op.ad;
-        const int n = S + op.ext;
-        if constexpr (sizeof(Acc) == 4) {
+    if constexpr (sizeof(Acc) == 4 && V == 0) {
+        int4* Vp = reinterpret_cast<int4*>(sm);
+        const int s4 = stride >> 2;
+        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+            const PassOpDev op = ops[o];
+            const int d4 = op.dst * s4, a4 = op.a * s4 + (op.ad >> 2);
+            const int n = S + op.ext;
             if (op.b < 0) {
-                for (int i = lane * 4; i < n; i += 128) sts4(d + i, lds4(a + i));
+                for (int k = lane; k * 4 < n; k += 32) Vp[d4 + k] = Vp[a4 + k];
                 continue;
             }
-            const Acc* bb = sm + (size_t)op.b * stride + (op.bd & ~3);
-            switch (op.bd & 3) {
-                case 0: op_rows<0>(d, a, bb, n, lane); break;
-                case 1: op_rows<1>(d, a, bb, n, lane); break;
-                case 2: op_rows<2>(d, a, bb, n, lane); break;
-                default: op_rows<3>(d, a, bb, n, lane); break;
+            rows_v_any<Acc>(Vp, d4, a4, op.b * s4, op.bd, n, lane);
+        }
+    } else if constexpr (sizeof(Acc) == 4) {
+        const uint32_t base = smem_u32(sm);
+        const uint32_t sb = static_cast<uint32_t>(stride) * 4u;
+        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+            const PassOpDev op = ops[o];
+            const uint32_t d = base + op.dst * sb, a = base + op.a * sb + op.ad * 4u;
+            const int n = S + op.ext;
+            if (op.b < 0) {
+                for (int i = lane * 4; i < n; i += 128) sts4u(d + i * 4u, lds4u(a + i * 4u));
+                continue;
             }
-        } else {
-            warp_merge(d, a, op.b >= 0 ? sm + (size_t)op.b * stride + op.bd : nullptr, n, lane);
+            rows_op_any<Acc>(d, a, base + op.b * sb, op.bd, n, lane);
+        }
+    } else {
+        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+            const PassOpDev op = ops[o];
+            warp_merge(sm + (size_t)op.dst * stride, sm + (size_t)op.a * stride + op.ad,
+                       op.b >= 0 ? sm + (size_t)op.b * stride + op.bd : nullptr, S + op.ext, lane);
         }
     }
 }
@@ -370,9 +456,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
 // ------------------------------------------------------------------ K1P
 // Specialised pass 0 for the common block: a width-32 Brady-Yong subtree
 // (every power-of-two block; all but at most one block of a Tweaked tree).
-// Its 5 levels' (t0, t1, shift) are compile-time constants (BYOp), so the
-// shared-memory addresses are immediate offsets and each shift's residue
-// mod 4 is static.  512 threads; warp w owns columns w and w + 16 at every
+// Its ops need no tables: (t0, t1, shift) follow from the column index with
+// a compile-time divisor per level.  512 threads; warp w owns columns w and w + 16 at every
 // level; lanes own 4 consecutive rows (16-byte shared accesses, lanes
 // contiguous: conflict-free).  Leaves live in slots [32, 64), level L
 // writes parity (5 - L) & 1, the block root ends in slots [0, 32).
@@ -382,24 +467,16 @@ constexpr int kBYSR = 300;      // slot stride: >= 256 + 31 + 12, multiple of 4,
 constexpr int kThreadsBY = 512;
 constexpr int kWarpsBY = kThreadsBY / 32;
 
-__host__ __device__ constexpr int rhu_c(int num, int den) { return (2 * num + den) / (2 * den); }
-
-template <int L, int T>
-struct BYOp {  // level L in 1..5 merges widths 2^(L-1) -> 2^L; T = block-local column
-    static constexpr int w = 1 << L, w0 = w >> 1, x0 = (T / w) * w, tl = T % w;
-    static constexpr int t0 = rhu_c(tl * (w0 - 1), w - 1);  // = t1 (both halves have width w0)
-    static constexpr int a = x0 + t0, b = x0 + w0 + t0, r = tl - t0;
-    static constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
-};
-
-template <class Acc, int L, int T>
-__device__ __forceinline__ void by_op(Acc* sm, int S, int lane) {
-    using O = BYOp<L, T>;
-    constexpr int M = O::r & 3;
-    const int n = S + kBYW - (1 << L);  // rows this level must produce (remaining halo)
-    Acc* d = sm + (O::dst + T) * kBYSR + lane * 4;
-    const Acc* a = sm + (O::src + O::a) * kBYSR + lane * 4;
-    const Acc* bb = sm + (O::src + O::b) * kBYSR + (O::r & ~3) + lane * 4;
+// Level L (1..5) merges widths 2^(L-1) -> 2^L.  For block-local column T
+// the children's slope t0 = t1 = rhu(tl (w0-1), w-1) (split.hpp:53-57) is
+// computed arithmetically (the divisor is a compile-time constant), so all
+// warps run the same short code path (no per-warp unrolled tables: those
+// thrashed the instruction cache).  Only the 4 residues of the shift are
+// specialised.
+// Variant 0 of a K1P op: C++ shared pointers, 3 predicated 128-row chunks.
+template <int M, class Acc>
+__device__ __forceinline__ void by_rows(Acc* __restrict__ d, const Acc* __restrict__ a, const Acc* __restrict__ bb,
+                                        int n, int lane) {
     int4 av[3], b0[3], b1[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
@@ -410,30 +487,52 @@ __device__ __forceinline__ void by_op(Acc* sm, int S, int lane) {
         }
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-        if (lane * 4 + 128 * c < n) {
-            const int bv[8] = {b0[c].x, b0[c].y, b0[c].z, b0[c].w,
-                               M ? b1[c].x : 0, M ? b1[c].y : 0, M ? b1[c].z : 0, 0};
-            sts4(d + 128 * c, make_int4(to_bits<Acc>(from_bits<Acc>(av[c].x) + from_bits<Acc>(bv[M + 0])),
-                                        to_bits<Acc>(from_bits<Acc>(av[c].y) + from_bits<Acc>(bv[M + 1])),
-                                        to_bits<Acc>(from_bits<Acc>(av[c].z) + from_bits<Acc>(bv[M + 2])),
-                                        to_bits<Acc>(from_bits<Acc>(av[c].w) + from_bits<Acc>(bv[M + 3]))));
-        }
+        if (lane * 4 + 128 * c < n) sts4(d + 128 * c, add_shift<M, Acc>(av[c], b0[c], M ? b1[c] : b0[c]));
 }
 
-template <class Acc, int L, int W = 0>
-__device__ __forceinline__ void by_level(Acc* sm, int S, int warp, int lane) {
-    if constexpr (W < kWarpsBY) {
-        if (warp == W) {
-            by_op<Acc, L, W>(sm, S, lane);
-            by_op<Acc, L, W + kWarpsBY>(sm, S, lane);
-        } else {
-            by_level<Acc, L, W + 1>(sm, S, warp, lane);
+template <class Acc, int L>
+__device__ __forceinline__ void by_level_v0(Acc* sm, int S, int warp, int lane) {
+    constexpr int w = 1 << L, w0 = w >> 1;
+    constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
+    const int n = S + kBYW - w;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int T = warp + h * kWarpsBY;
+        const int tl = T & (w - 1), x0 = T & ~(w - 1);
+        const int t0 = (2 * tl * (w0 - 1) + (w - 1)) / (2 * (w - 1));
+        const int r = tl - t0;
+        Acc* d = sm + (dst + T) * kBYSR + lane * 4;
+        const Acc* a = sm + (src + x0 + t0) * kBYSR + lane * 4;
+        const Acc* bb = sm + (src + x0 + w0 + t0) * kBYSR + (r & ~3) + lane * 4;
+        switch (r & 3) {
+            case 0: by_rows<0>(d, a, bb, n, lane); break;
+            case 1: by_rows<1>(d, a, bb, n, lane); break;
+            case 2: by_rows<2>(d, a, bb, n, lane); break;
+            default: by_rows<3>(d, a, bb, n, lane); break;
         }
     }
 }
 
+template <class Acc, int L>
+__device__ __forceinline__ void by_level(Acc* sm, int S, int warp, int lane) {
+    constexpr int w = 1 << L, w0 = w >> 1;
+    constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
+    const int n = S + kBYW - w;  // rows this level must produce (remaining halo)
+    const uint32_t base = smem_u32(sm);
+    constexpr uint32_t sb = kBYSR * 4u;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int T = warp + h * kWarpsBY;
+        const int tl = T & (w - 1), x0 = T & ~(w - 1);
+        const int t0 = (2 * tl * (w0 - 1) + (w - 1)) / (2 * (w - 1));
+        const int r = tl - t0;
+        rows_op_any<Acc>(base + (dst + T) * sb, base + (src + x0 + t0) * sb, base + (src + x0 + w0 + t0) * sb, r, n,
+                         lane);
+    }
+}
+
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
-template <class In, class Acc>
+template <class In, class Acc, int V>
 __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
                                                           long long img_stride, int img0, QuadSet qs, int W, int H,
                                                           int ld, int S, const int* __restrict__ bx0,
@@ -503,15 +602,27 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         }
     }
     __syncthreads();
-    by_level<Acc, 1>(sm, S, warp, lane);
-    __syncthreads();
-    by_level<Acc, 2>(sm, S, warp, lane);
-    __syncthreads();
-    by_level<Acc, 3>(sm, S, warp, lane);
-    __syncthreads();
-    by_level<Acc, 4>(sm, S, warp, lane);
-    __syncthreads();
-    by_level<Acc, 5>(sm, S, warp, lane);
+    if constexpr (V == 0) {
+        by_level_v0<Acc, 1>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 2>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 4>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 5>(sm, S, warp, lane);
+    } else {
+        by_level<Acc, 1>(sm, S, warp, lane);
+        __syncthreads();
+        by_level<Acc, 2>(sm, S, warp, lane);
+        __syncthreads();
+        by_level<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level<Acc, 4>(sm, S, warp, lane);
+        __syncthreads();
+        by_level<Acc, 5>(sm, S, warp, lane);
+    }
     __syncthreads();
     const int rows_out = min(S, H - s0);
     Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
@@ -535,7 +646,7 @@ size_t k1_by32_smem_bytes() { return (2 * kBYW * kBYSR + 16) * 4; }
 // reference layout hough[s*W + t] (transform.cpp:80-83).
 constexpr int kThreads2 = 512;
 
-template <class Acc, class Out>
+template <class Acc, class Out, int V>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
@@ -549,6 +660,11 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     const int slot = blockIdx.z;
     const Acc* __restrict__ in = src + (size_t)slot * slot_elems;
 
+    // 0. stage the tile's merge ops in shared memory (after the slots)
+    PassOpDev* sops = reinterpret_cast<PassOpDev*>(sm + (size_t)ps.max_slots * L + 16);
+    const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
+    for (int k = tid; k < nops * 2; k += kThreads2)
+        reinterpret_cast<int4*>(sops)[k] = reinterpret_cast<const int4*>(ps.ops + op0)[k];
     // 1. windows of the input columns
     for (int l = warp; l < tile.load_cnt; l += kWarps) {
         const int4 ld4 = ps.loads[tile.load_beg + l];
@@ -558,8 +674,8 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     // 2. merge levels
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
-        run_step<Acc, kWarps>(sm, L, ps.ops, ps.step_offs[tile.step_beg + k], ps.step_offs[tile.step_beg + k + 1], S,
-                              warp, lane);
+        run_step<Acc, kWarps, V>(sm, L, sops, ps.step_offs[tile.step_beg + k] - op0,
+                              ps.step_offs[tile.step_beg + k + 1] - op0, S, warp, lane);
     }
     __syncthreads();
     // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)
@@ -643,7 +759,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
     if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
-            auto kb = k1_by32<In, Acc>;
+            auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 1>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
@@ -668,8 +784,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         const bool final_pass = (p == g.npasses - 1);
         const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
-        const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L);
-        auto k2 = k2_pass<Acc, Out>;
+        const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
+        auto k2 = g.k2_variant == 0 ? k2_pass<Acc, Out, 0> : k2_pass<Acc, Out, 1>;
         cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
         k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
@@ -692,9 +808,10 @@ size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_
     return k1_ops_offset(acc_dtype, max_width, sr) + 64;  // two slot buffers + vector-read slack
 }
 
-size_t k2_smem_bytes(int acc_dtype, int max_slots, int L) {
+size_t k2_smem_bytes(int acc_dtype, int max_slots, int L, int max_tile_ops) {
     const size_t esz = acc_dtype == kI64 ? 8 : 4;
-    return (static_cast<size_t>(max_slots) * L + 16) * esz;  // +16: vector-merge read slack
+    // slots, +16 elements of vector-merge read slack, then the staged ops
+    return (static_cast<size_t>(max_slots) * L + 16) * esz + static_cast<size_t>(max_tile_ops) * sizeof(PassOpDev);
 }
 
 int launch_group(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* ctx) {

@@ -52,6 +52,7 @@ struct PassDev {
     int S;       // rows per row tile
     int L;       // smem row capacity of a slot (>= S + max_ext, odd)
     int max_slots;
+    int max_tile_ops;  // most merge ops in one tile (staged in shared memory)
 };
 
 struct GroupLaunch {
@@ -72,6 +73,8 @@ struct GroupLaunch {
     const int4* blocks;
     int nby;            // width-32 Brady-Yong blocks for the specialised K1P (4-byte accumulators)
     const int* by_x0;
+    int k1p_variant;    // experiment switches (FHT_K1P_VARIANT, FHT_K2_VARIANT)
+    int k2_variant;
     const ShapeHdr* shapes;
     const int* step_offs;
     const PassOpDev* k1_ops;  // per-shape ops, slots pre-offset by buffer parity
@@ -87,7 +90,7 @@ struct GroupLaunch {
 };
 
 size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps);
-size_t k2_smem_bytes(int acc_dtype, int max_slots, int L);
+size_t k2_smem_bytes(int acc_dtype, int max_slots, int L, int max_tile_ops);
 // Launch every kernel of one orientation group / chunk on `stream`.
 // Returns the number of kernel launches, or -1 on an unsupported type combination.
 // `hook(ctx, kind)` (optional) runs after each launch; kind 1 = K1 (generic
