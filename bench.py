@@ -32,7 +32,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2411_07351_b200 import fht, workloads  # noqa: E402
+from paper_2411_07351_b200 import fht, shard, workloads  # noqa: E402
 from paper_2411_07351_b200._lib import check, lib  # noqa: E402
 
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
@@ -42,7 +42,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -85,7 +85,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
             return
@@ -94,9 +94,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def stop(self, window=None):
+        """Summarise the samples taken inside `window` = (t0, t1) wall-clock
+        (the timed region); all samples if fewer than 2 fall inside."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -108,7 +110,13 @@ class ClockSampler:
             self.thread.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        scope = "all samples"
+        if window is not None:
+            inside = [(t, ln) for t, ln in lines if window[0] - 0.05 <= t <= window[1] + 0.05]
+            if len(inside) >= 2:
+                lines, scope = inside, "timed region"
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -121,7 +129,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "scope": scope}
 
 
 # ---------------------------------------------------------------- CPU arm
@@ -209,8 +217,21 @@ def run_ours(args):
     c = workloads.CONFIGS[args.config]
     strategy = 0 if args.strategy == "simple" else 1
 
-    imgs = workloads.make_images(args.config, c.batch, offset=rank * c.batch)  # this rank's shard
-    plan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=list(c.quadrants),
+    if c.batch == 1 and ws > 1:
+        # one large image: split its quadrants over the ranks (strong scaling)
+        my_q = shard.quadrant_shard(ws, rank, c.quadrants)
+        imgs = workloads.make_images(args.config, 1)
+        scaling = "strong"
+        sums_per_step = workloads.nominal_sums(args.config)
+    else:
+        # a batch per rank, no collective on the data path (weak scaling)
+        my_q = list(c.quadrants)
+        imgs = workloads.make_images(args.config, c.batch, offset=rank * c.batch)
+        scaling = "weak"
+        sums_per_step = workloads.nominal_sums(args.config) * ws
+    if not my_q:  # more ranks than quadrants: this rank idles but joins the timing
+        my_q = None
+    plan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=my_q or [c.quadrants[0]],
                     batch=c.batch, device=local)
     x = torch.from_numpy(imgs).to(dev)
     out = plan.alloc_outputs()
@@ -224,6 +245,8 @@ def run_ours(args):
         ptrs[i] = out[q].data_ptr() if q in out else None
 
     def step():
+        if my_q is None:
+            return
         check(lib().fht_execute(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
                                 ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
                                 ctypes.c_void_p(stream.cuda_stream)))
@@ -234,10 +257,17 @@ def run_ours(args):
         flush.fill_(1)
         step()
     torch.cuda.synchronize()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 0.5:  # untimed soak: clocks settle under load
+        for _ in range(8):
+            flush.fill_(1)
+            step()
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_wall0 = time.time()
     for s, e in evs:
         flush.fill_(1)  # L2 flush, outside the timed interval
         s.record(stream)
@@ -247,14 +277,14 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = sampler.stop()
+    t_wall1 = time.time()
+    clocks = sampler.stop((t_wall0, t_wall1))
     total_ms = sum(s.elapsed_time(e) for s, e in evs)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    sums_per_step = workloads.nominal_sums(args.config) * ws
     value = sums_per_step / (ms_per_step * 1e-3) / 1e9
 
     # Per-kernel live timing (events between launches, same stream) for the roofline.
@@ -304,7 +334,7 @@ def run_ours(args):
 
     # e2e through the C-ABI host-buffer call (pinned host memory).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and my_q is not None:
         h_in = torch.from_numpy(imgs).pin_memory()
         h_out = {q: torch.empty(out[q].shape, dtype=out[q].dtype).pin_memory() for q in out}
         optrs = [h_out[q].data_ptr() if q in h_out else None for q in fht.QUADRANTS]
@@ -334,13 +364,14 @@ def run_ours(args):
         line = {
             "metric": "FHT Gsums/s", "value": round(value, 3), "unit": "Gsums/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": c.acc,
+            "scaling": scaling, "vs_baseline": None, "dtype": c.acc,
             "data": "synthetic (seeded, BASELINE.json config shapes/distributions)",
             "config": {"workload": args.config, "description": c.description, "n": c.n,
                        "images_per_gpu": c.batch, "quadrants": len(c.quadrants), "strategy": args.strategy,
-                       "in_dtype": c.dtype, "acc_dtype": c.acc, "parallelism": f"batch-shard x{ws}",
+                       "in_dtype": c.dtype, "acc_dtype": c.acc,
+                       "parallelism": (f"quadrant-split x{ws}" if scaling == "strong" else f"batch-shard x{ws}"),
                        "l2": "flushed between timed steps (512 MiB write, untimed)"},
-            "images_per_s": round(c.batch * ws / (ms_per_step * 1e-3), 1),
+            "images_per_s": round((c.batch * ws if scaling == "weak" else 1) / (ms_per_step * 1e-3), 1),
             "hbm_gbs_step": round(step_gbs, 1),
             "roofline": roofline,
             "cpu_baseline": cpu,

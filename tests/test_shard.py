@@ -1,0 +1,79 @@
+"""CPU (gloo, world_size 2) tests of the multi-GPU host logic: every image is
+transformed by exactly one rank, and gathering the per-rank results
+reproduces the single-process transform of the whole batch (the transform
+here is the oracle, since this container has no GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_07351_b200.shard import QUADRANTS, batch_shard, gather_to_root, max_over_ranks, quadrant_shard
+
+
+def test_batch_shard_covers_exactly_once():
+    for n in (0, 1, 7, 256, 257):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                s = batch_shard(n, world, r)
+                seen.extend(range(s.start, s.start + s.count))
+            assert seen == list(range(n))
+            counts = [batch_shard(n, world, r).count for r in range(world)]
+            assert max(counts) - min(counts) <= 1
+
+
+def test_quadrant_shard():
+    assert [quadrant_shard(4, r) for r in range(4)] == [[q] for q in QUADRANTS]
+    assert sorted(sum((quadrant_shard(2, r) for r in range(2)), [])) == sorted(QUADRANTS)
+    assert sum((quadrant_shard(8, r) for r in range(8)), []) == list(QUADRANTS)
+    with pytest.raises(ValueError):
+        batch_shard(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+
+    rng = np.random.default_rng(5)
+    imgs = rng.integers(0, 256, (6, 23, 31), dtype=np.uint8)  # same batch on every rank
+    sh = batch_shard(len(imgs), world, rank)
+    res = []
+    for i in range(sh.start, sh.start + sh.count):
+        q, _ = oracle.fht2d_quadrants(imgs[i], oracle.TWEAKED, dtype=np.int32)
+        res.append(np.stack([q["horiz_pos"], q["horiz_neg"]]))
+    local = torch.from_numpy(np.stack(res))
+    full = gather_to_root(local)
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        np.save(out_path, full.numpy())
+        assert t == float(world)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_matches_single_process(tmp_path):
+    world, out = 2, tmp_path / "gathered.npy"
+    mp.spawn(_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
+    import oracle
+
+    rng = np.random.default_rng(5)
+    imgs = rng.integers(0, 256, (6, 23, 31), dtype=np.uint8)
+    ref = []
+    for i in range(6):
+        q, _ = oracle.fht2d_quadrants(imgs[i], oracle.TWEAKED, dtype=np.int32)
+        ref.append(np.stack([q["horiz_pos"], q["horiz_neg"]]))
+    np.testing.assert_array_equal(np.load(out), np.stack(ref))
