@@ -309,7 +309,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const int W = horizontal ? w : h, H = horizontal ? h : w;
         // Fused-pass tiles: shrink the tile width until every pass gets a
         // reasonable row tile in the shared-memory budget.
-        const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 100, 16, 220)) * 1024;
+        const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 105, 16, 220)) * 1024;
         const int levels = env_int("FHT_PASS_LEVELS", 4, 1, 8);
         int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
         for (;;) {
@@ -412,8 +412,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.blocks = g.dt.blocks;
             L.nby = g.nby;
             L.by_x0 = g.dt.by_x0;
-            L.k1p_variant = env_int("FHT_K1P_VARIANT", 0, 0, 1);
-            L.k2_variant = env_int("FHT_K2_VARIANT", 1, 0, 1);
+            L.k1p_variant = env_int("FHT_K1P_VARIANT", 2, 0, 2);  // 2: levels 1-2 in registers
             L.shapes = g.dt.shapes;
             L.step_offs = g.dt.step_offs;
             L.k1_ops = g.dt.k1_ops;

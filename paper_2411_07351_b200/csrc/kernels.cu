@@ -172,42 +172,6 @@ __device__ __forceinline__ void rows_op(uint32_t d, uint32_t a, uint32_t bb, int
     }
 }
 
-// Same op with int4 indices into the shared array (the compiler keeps one
-// shared base and schedules the loads freely): rows [0, n) of
-// V[d4..] = V[a4..] + (V[b4..] shifted by M).  Three predicated 128-row
-// chunks per iteration, every load of an iteration before its stores.
-template <int M, class Acc>
-__device__ __forceinline__ void rows_v(int4* __restrict__ V, int d4, int a4, int b4, int n, int lane) {
-    for (int i0 = lane; i0 * 4 < n; i0 += 96) {
-        int4 av[3], b0[3], b1[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int k = i0 + 32 * c;
-            if (k * 4 < n) {
-                av[c] = V[a4 + k];
-                b0[c] = V[b4 + k];
-                if (M) b1[c] = V[b4 + k + 1];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int k = i0 + 32 * c;
-            if (k * 4 < n) V[d4 + k] = add_shift<M, Acc>(av[c], b0[c], M ? b1[c] : b0[c]);
-        }
-    }
-}
-
-template <class Acc>
-__device__ __forceinline__ void rows_v_any(int4* V, int d4, int a4, int b4, int bd, int n, int lane) {
-    b4 += bd >> 2;
-    switch (bd & 3) {
-        case 0: rows_v<0, Acc>(V, d4, a4, b4, n, lane); break;
-        case 1: rows_v<1, Acc>(V, d4, a4, b4, n, lane); break;
-        case 2: rows_v<2, Acc>(V, d4, a4, b4, n, lane); break;
-        default: rows_v<3, Acc>(V, d4, a4, b4, n, lane); break;
-    }
-}
-
 template <class Acc>
 __device__ __forceinline__ void rows_op_any(uint32_t d, uint32_t a, uint32_t b, int bd, int n, int lane) {
     const uint32_t bb = b + static_cast<uint32_t>(bd & ~3) * 4u;
@@ -296,23 +260,10 @@ __device__ __forceinline__ void warp_merge_any(Acc* d, const Acc* a, const Acc* 
 //   i < S + ext (b < 0: copy).
 // a and dst are 16-byte aligned (ad % 4 == 0); b is read from its aligned
 // base and the warp-uniform residue bd & 3 selects a specialised loop.
-template <class Acc, int NWARPS, int V = 1>
+template <class Acc, int NWARPS>
 __device__ __forceinline__ void run_step(Acc* sm, int stride, const PassOpDev* __restrict__ ops, int o_beg,
                                          int o_end, int S, int warp, int lane) {
-    if constexpr (sizeof(Acc) == 4 && V == 0) {
-        int4* Vp = reinterpret_cast<int4*>(sm);
-        const int s4 = stride >> 2;
-        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
-            const PassOpDev op = ops[o];
-            const int d4 = op.dst * s4, a4 = op.a * s4 + (op.ad >> 2);
-            const int n = S + op.ext;
-            if (op.b < 0) {
-                for (int k = lane; k * 4 < n; k += 32) Vp[d4 + k] = Vp[a4 + k];
-                continue;
-            }
-            rows_v_any<Acc>(Vp, d4, a4, op.b * s4, op.bd, n, lane);
-        }
-    } else if constexpr (sizeof(Acc) == 4) {
+    if constexpr (sizeof(Acc) == 4) {
         const uint32_t base = smem_u32(sm);
         const uint32_t sb = static_cast<uint32_t>(stride) * 4u;
         for (int o = o_beg + warp; o < o_end; o += NWARPS) {
@@ -490,10 +441,10 @@ __device__ __forceinline__ void by_rows(Acc* __restrict__ d, const Acc* __restri
         if (lane * 4 + 128 * c < n) sts4(d + 128 * c, add_shift<M, Acc>(av[c], b0[c], M ? b1[c] : b0[c]));
 }
 
-template <class Acc, int L>
+template <class Acc, int L, int F = 0>
 __device__ __forceinline__ void by_level_v0(Acc* sm, int S, int warp, int lane) {
     constexpr int w = 1 << L, w0 = w >> 1;
-    constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
+    constexpr int src = ((6 - L + F) & 1) * kBYW, dst = ((5 - L + F) & 1) * kBYW;
     const int n = S + kBYW - w;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -513,21 +464,52 @@ __device__ __forceinline__ void by_level_v0(Acc* sm, int S, int warp, int lane) 
     }
 }
 
-template <class Acc, int L>
-__device__ __forceinline__ void by_level(Acc* sm, int S, int warp, int lane) {
-    constexpr int w = 1 << L, w0 = w >> 1;
-    constexpr int src = ((6 - L) & 1) * kBYW, dst = ((5 - L) & 1) * kBYW;
-    const int n = S + kBYW - w;  // rows this level must produce (remaining halo)
-    const uint32_t base = smem_u32(sm);
-    constexpr uint32_t sb = kBYSR * 4u;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int T = warp + h * kWarpsBY;
-        const int tl = T & (w - 1), x0 = T & ~(w - 1);
-        const int t0 = (2 * tl * (w0 - 1) + (w - 1)) / (2 * (w - 1));
-        const int r = tl - t0;
-        rows_op_any<Acc>(base + (dst + T) * sb, base + (src + x0 + t0) * sb, base + (src + x0 + w0 + t0) * sb, r, n,
-                         lane);
+// Levels 1 and 2 of a width-32 block fused in registers: item (g, j) reads
+// the leaves of columns 4g..4g+3, rows 4j..4j+7 (two aligned 16-byte loads
+// per column), forms both level-1 pairs (shift 0/1) and the level-2 width-4
+// merge (t0 = 0,0,1,1; shift 0,1,1,2 -- BYOp at L = 1, 2) and stores rows
+// 4j..4j+3 of the 4 level-2 columns.  Leaves: slots [32, 64); level 2: slots
+// [0, 32).  Rows produced: [0, S + 28) (the halo levels 3..5 still need).
+template <class Acc>
+__device__ __forceinline__ int4 add4(int4 a, int4 b) {
+    return make_int4(to_bits<Acc>(from_bits<Acc>(a.x) + from_bits<Acc>(b.x)),
+                     to_bits<Acc>(from_bits<Acc>(a.y) + from_bits<Acc>(b.y)),
+                     to_bits<Acc>(from_bits<Acc>(a.z) + from_bits<Acc>(b.z)),
+                     to_bits<Acc>(from_bits<Acc>(a.w) + from_bits<Acc>(b.w)));
+}
+// rows k..k+3 of a column held as two vectors (rows 0..3, 4..7) shifted by K
+template <int K>
+__device__ __forceinline__ int4 shifted(int4 lo, int4 hi) {
+    const int v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    return make_int4(v[K], v[K + 1], v[K + 2], v[K + 3]);
+}
+
+template <class Acc>
+__device__ __forceinline__ void by_level12(Acc* sm, int S, int tid) {
+    const int nchunk = (S + kBYW - 4 + 3) >> 2;  // row chunks of 4 the level-2 output needs
+    const int items = 8 * nchunk;
+    const int4* V = reinterpret_cast<const int4*>(sm);
+    int4* O = reinterpret_cast<int4*>(sm);
+    constexpr int s4 = kBYSR / 4;
+    for (int it = tid; it < items; it += kThreadsBY) {
+        const int g = it / nchunk, j = it - g * nchunk;  // lanes over row chunks: conflict-free
+        const int c0 = (kBYW + 4 * g) * s4 + j;  // leaves of column 4g, chunk j
+        // pair (4g, 4g+1) -> level-1 columns p0 (shift 0), p1 (shift 1), rows j*4 .. j*4+6
+        const int4 a0 = V[c0], a1 = V[c0 + 1], b0 = V[c0 + s4], b1 = V[c0 + s4 + 1];
+        const int4 e0 = V[c0 + 2 * s4], e1 = V[c0 + 2 * s4 + 1], f0 = V[c0 + 3 * s4], f1 = V[c0 + 3 * s4 + 1];
+        // level 1 (rows 0..3 and 4..7 of each output, from the two vectors)
+        const int4 p0l = add4<Acc>(a0, b0), p0h = add4<Acc>(a1, b1);
+        const int4 p1l = add4<Acc>(a0, shifted<1>(b0, b1)), p1h = add4<Acc>(a1, shifted<1>(b1, b1));
+        const int4 q0l = add4<Acc>(e0, f0), q0h = add4<Acc>(e1, f1);
+        const int4 q1l = add4<Acc>(e0, shifted<1>(f0, f1)), q1h = add4<Acc>(e1, shifted<1>(f1, f1));
+        // level 2: o0 = p0 + q0, o1 = p0 + q0[+1], o2 = p1 + q1[+1], o3 = p1 + q1[+2]
+        const int d0 = (4 * g) * s4 + j;
+        O[d0] = add4<Acc>(p0l, q0l);
+        O[d0 + s4] = add4<Acc>(p0l, shifted<1>(q0l, q0h));
+        O[d0 + 2 * s4] = add4<Acc>(p1l, shifted<1>(q1l, q1h));
+        O[d0 + 3 * s4] = add4<Acc>(p1l, shifted<2>(q1l, q1h));
+        (void)p0h;
+        (void)p1h;
     }
 }
 
@@ -602,7 +584,15 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         }
     }
     __syncthreads();
-    if constexpr (V == 0) {
+    if constexpr (V == 2) {
+        by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
+        __syncthreads();
+        by_level_v0<Acc, 3, 1>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 4, 1>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_v0<Acc, 5, 1>(sm, S, warp, lane);  // block root -> slots [32, 64)
+    } else {
         by_level_v0<Acc, 1>(sm, S, warp, lane);
         __syncthreads();
         by_level_v0<Acc, 2>(sm, S, warp, lane);
@@ -612,25 +602,16 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         by_level_v0<Acc, 4>(sm, S, warp, lane);
         __syncthreads();
         by_level_v0<Acc, 5>(sm, S, warp, lane);
-    } else {
-        by_level<Acc, 1>(sm, S, warp, lane);
-        __syncthreads();
-        by_level<Acc, 2>(sm, S, warp, lane);
-        __syncthreads();
-        by_level<Acc, 3>(sm, S, warp, lane);
-        __syncthreads();
-        by_level<Acc, 4>(sm, S, warp, lane);
-        __syncthreads();
-        by_level<Acc, 5>(sm, S, warp, lane);
     }
     __syncthreads();
     const int rows_out = min(S, H - s0);
     Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
     const bool al = ((ld | s0) & 3) == 0;
+    const Acc* root = sm + (V == 2 ? kBYW * kBYSR : 0);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int c = warp + h * kWarpsBY;
-        warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, sm + c * kBYSR, rows_out, al, lane);
+        warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, root + c * kBYSR, rows_out, al, lane);
     }
 }
 
@@ -646,7 +627,7 @@ size_t k1_by32_smem_bytes() { return (2 * kBYW * kBYSR + 16) * 4; }
 // reference layout hough[s*W + t] (transform.cpp:80-83).
 constexpr int kThreads2 = 512;
 
-template <class Acc, class Out, int V>
+template <class Acc, class Out>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
@@ -674,7 +655,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     // 2. merge levels
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
-        run_step<Acc, kWarps, V>(sm, L, sops, ps.step_offs[tile.step_beg + k] - op0,
+        run_step<Acc, kWarps>(sm, L, sops, ps.step_offs[tile.step_beg + k] - op0,
                               ps.step_offs[tile.step_beg + k + 1] - op0, S, warp, lane);
     }
     __syncthreads();
@@ -759,7 +740,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
     if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
-            auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 1>;
+            auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 2>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
@@ -785,7 +766,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
-        auto k2 = g.k2_variant == 0 ? k2_pass<Acc, Out, 0> : k2_pass<Acc, Out, 1>;
+        auto k2 = k2_pass<Acc, Out>;
         cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
         k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);

@@ -73,8 +73,7 @@ struct GroupLaunch {
     const int4* blocks;
     int nby;            // width-32 Brady-Yong blocks for the specialised K1P (4-byte accumulators)
     const int* by_x0;
-    int k1p_variant;    // experiment switches (FHT_K1P_VARIANT, FHT_K2_VARIANT)
-    int k2_variant;
+    int k1p_variant;    // 2 (default): levels 1-2 in registers; 0: all levels in shared memory
     const ShapeHdr* shapes;
     const int* step_offs;
     const PassOpDev* k1_ops;  // per-shape ops, slots pre-offset by buffer parity
