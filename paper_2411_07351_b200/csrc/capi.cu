@@ -96,10 +96,17 @@ struct Group {
     int ld = 0, S = 0, sr = 0, nbuf = 0;
     int nblocks = 0, nby = 0;
     bool use_by32 = false;
+    std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
     size_t slot_bytes = 0;
 };
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+int env_int(const char* name, int def, int lo, int hi) {
+    if (const char* e = std::getenv(name)) return std::max(lo, std::min(hi, std::atoi(e)));
+    return def;
+}
+
 
 }  // namespace
 
@@ -201,7 +208,7 @@ void upload(Group& g) {
     const size_t o_steps = put(step_offs.data(), step_offs.size() * sizeof(int));
     const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(fhtb::PassOp));
     struct PassOff {
-        size_t tiles, loads, steps, ops, stores;
+        size_t tiles, loads, steps, ops, stores, bops;
     };
     std::vector<PassOff> o_passes;
     for (const auto& ps : sp.passes) {
@@ -217,6 +224,19 @@ void upload(Group& g) {
         std::vector<int2> stores;
         for (const auto& st : ps.stores) stores.push_back(make_int2(st.slot, st.gcol));
         o.stores = put(stores.data(), stores.size() * sizeof(int2));
+        // ops baked into shared byte offsets for the 4-byte kernel path
+        {
+            const int64_t L = g.pass_L[o_passes.size()], S = g.pass_S[o_passes.size()];
+            std::vector<int4> bops;
+            for (const auto& op : ps.ops) {
+                const int64_t d = op.dst * L * 4, a = (op.a * L + op.ad) * 4;
+                const int64_t b = op.b < 0 ? -1 : ((op.b * L + (op.bd & ~3)) * 4) | (op.bd & 3);
+                if (d > INT32_MAX || a > INT32_MAX || b > INT32_MAX) throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
+                bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(a), static_cast<int>(b),
+                                         static_cast<int>(S + op.ext)));
+            }
+            o.bops = put(bops.data(), bops.size() * sizeof(int4));
+        }
         o_passes.push_back(o);
     }
     blob.resize(blob.size() + 16);
@@ -236,6 +256,10 @@ void upload(Group& g) {
         d.step_offs = reinterpret_cast<const int*>(base + o.steps);
         d.ops = reinterpret_cast<const fhtb::PassOpDev*>(base + o.ops);
         d.stores = reinterpret_cast<const int2*>(base + o.stores);
+        d.bops = reinterpret_cast<const int4*>(base + o.bops);
+        d.S = g.pass_S[i];
+        d.L = g.pass_L[i];
+        d.pair_loads = env_int("FHT_K2_PAIR_LOADS", 0, 0, 1);
         d.ntiles = static_cast<int>(sp.passes[i].tiles.size());
         d.max_slots = sp.passes[i].max_slots;
         d.max_tile_ops = 0;
@@ -246,10 +270,6 @@ void upload(Group& g) {
     }
 }
 
-int env_int(const char* name, int def, int lo, int hi) {
-    if (const char* e = std::getenv(name)) return std::max(lo, std::min(hi, std::atoi(e)));
-    return def;
-}
 
 // Rows per K2 row tile for a pass: as many as fit `budget` bytes of shared
 // memory (max_slots slots of S + max_ext rows), capped at H; multiples of 32.
@@ -344,21 +364,22 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         g->nbuf = g->sp.root_is_block ? 0 : (g->sp.passes.size() > 1 ? 2 : 1);
         g->use_by32 = acc_sz == 4 && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
         g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
-        upload(*g);
-        for (size_t i = 0; i < g->dt.passes.size(); ++i) {
-            auto& d = g->dt.passes[i];
-            d.S = pass_rows(g->sp.passes[i], H, acc_sz, budget);
+        for (size_t i = 0; i < g->sp.passes.size(); ++i) {
+            int S2 = std::min(256, pass_rows(g->sp.passes[i], H, acc_sz, budget));
             {  // balance the row tiles
-                const int nt = (H + d.S - 1) / std::max(1, d.S);
-                d.S = std::min(d.S, ((H + nt - 1) / nt + 7) & ~7);
-                if (d.S > H) d.S = H;
+                const int nt = (H + S2 - 1) / std::max(1, S2);
+                S2 = std::min(S2, ((H + nt - 1) / nt + 7) & ~7);
+                if (S2 > H) S2 = H;
             }
             // slot capacity: window + vector-merge slack, a multiple of 4 rows
             // (16-byte aligned slots) with L/4 odd (spreads the transposed
             // root stores over the banks)
-            d.L = (d.S + g->sp.passes[i].max_ext + 12 + 3) & ~3;
-            if (((d.L >> 2) & 1) == 0) d.L += 4;
+            int L2 = (S2 + g->sp.passes[i].max_ext + 12 + 3) & ~3;
+            if (((L2 >> 2) & 1) == 0) L2 += 4;
+            g->pass_S.push_back(S2);
+            g->pass_L.push_back(L2);
         }
+        upload(*g);
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);

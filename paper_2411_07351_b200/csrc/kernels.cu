@@ -263,26 +263,64 @@ __device__ __forceinline__ void warp_merge_any(Acc* d, const Acc* a, const Acc* 
 template <class Acc, int NWARPS>
 __device__ __forceinline__ void run_step(Acc* sm, int stride, const PassOpDev* __restrict__ ops, int o_beg,
                                          int o_end, int S, int warp, int lane) {
-    if constexpr (sizeof(Acc) == 4) {
-        const uint32_t base = smem_u32(sm);
-        const uint32_t sb = static_cast<uint32_t>(stride) * 4u;
-        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
-            const PassOpDev op = ops[o];
-            const uint32_t d = base + op.dst * sb, a = base + op.a * sb + op.ad * 4u;
-            const int n = S + op.ext;
-            if (op.b < 0) {
-                for (int i = lane * 4; i < n; i += 128) sts4u(d + i * 4u, lds4u(a + i * 4u));
-                continue;
-            }
-            rows_op_any<Acc>(d, a, base + op.b * sb, op.bd, n, lane);
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const PassOpDev op = ops[o];
+        warp_merge(sm + (size_t)op.dst * stride, sm + (size_t)op.a * stride + op.ad,
+                   op.b >= 0 ? sm + (size_t)op.b * stride + op.bd : nullptr, S + op.ext, lane);
+    }
+}
+
+// 4-byte path with ops baked on the host into 16-byte records of shared
+// byte offsets: {dst, a (+ad), b aligned base | (bd & 3)  (-1: copy), rows}.
+template <class Acc, int NWARPS>
+__device__ __forceinline__ void run_step_baked(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
+                                               int warp, int lane) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 op = ops[o];
+        const uint32_t d = base + static_cast<uint32_t>(op.x), a = base + static_cast<uint32_t>(op.y);
+        const int n = op.w;
+        if (op.z < 0) {
+            for (int i = lane * 4; i < n; i += 128) sts4u(d + i * 4u, lds4u(a + i * 4u));
+            continue;
         }
-    } else {
-        for (int o = o_beg + warp; o < o_end; o += NWARPS) {
-            const PassOpDev op = ops[o];
-            warp_merge(sm + (size_t)op.dst * stride, sm + (size_t)op.a * stride + op.ad,
-                       op.b >= 0 ? sm + (size_t)op.b * stride + op.bd : nullptr, S + op.ext, lane);
+        const uint32_t bb = base + static_cast<uint32_t>(op.z & ~15);
+        switch (op.z & 3) {
+            case 0: rows_op<0, Acc>(d, a, bb, n, lane); break;
+            case 1: rows_op<1, Acc>(d, a, bb, n, lane); break;
+            case 2: rows_op<2, Acc>(d, a, bb, n, lane); break;
+            default: rows_op<3, Acc>(d, a, bb, n, lane); break;
         }
     }
+}
+
+// Two K2 windows per warp at once (4-byte types): the aligned, pre-wrap part
+// of each with up to 6 16-byte loads in flight per lane, then the remainder
+// (after the wrap point) with unrolled scalar loads.
+template <class Acc>
+__device__ __forceinline__ void warp_load_window_pair(Acc* d0, const Acc* __restrict__ c0, int st0, int n0, Acc* d1,
+                                                      const Acc* __restrict__ c1, int st1, int n1, int H,
+                                                      int lane) {
+    const int run0 = (st0 & 3) ? 0 : (min(n0, H - st0) & ~3);
+    const int run1 = (d1 && !(st1 & 3)) ? (min(n1, H - st1) & ~3) : 0;
+    const int4* __restrict__ s0p = reinterpret_cast<const int4*>(c0 + st0);
+    const int4* __restrict__ s1p = reinterpret_cast<const int4*>(c1 + (d1 ? st1 : 0));
+    for (int k0 = 0; k0 < max(run0, run1) / 4; k0 += 64) {
+        int4 v0[2], v1[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int k = k0 + lane + 32 * c;
+            if (4 * k < run0) v0[c] = s0p[k];
+            if (4 * k < run1) v1[c] = s1p[k];
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int k = k0 + lane + 32 * c;
+            if (4 * k < run0) sts4(d0 + 4 * k, v0[c]);
+            if (4 * k < run1) sts4(d1 + 4 * k, v1[c]);
+        }
+    }
+    if (run0 < n0) warp_load_window(d0 + run0, c0, wrap_any(st0 + run0, H), n0 - run0, H, lane);
+    if (d1 && run1 < n1) warp_load_window(d1 + run1, c1, wrap_any(st1 + run1, H), n1 - run1, H, lane);
 }
 
 // Column store smem -> global, rows [0, n): 16-byte stores when the global
@@ -643,20 +681,40 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
 
     // 0. stage the tile's merge ops in shared memory (after the slots)
     PassOpDev* sops = reinterpret_cast<PassOpDev*>(sm + (size_t)ps.max_slots * L + 16);
+    int4* sbops = reinterpret_cast<int4*>(sops);
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
-    for (int k = tid; k < nops * 2; k += kThreads2)
-        reinterpret_cast<int4*>(sops)[k] = reinterpret_cast<const int4*>(ps.ops + op0)[k];
+    if constexpr (sizeof(Acc) == 4) {
+        for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
+    } else {
+        for (int k = tid; k < nops * 2; k += kThreads2)
+            reinterpret_cast<int4*>(sops)[k] = reinterpret_cast<const int4*>(ps.ops + op0)[k];
+    }
     // 1. windows of the input columns
-    for (int l = warp; l < tile.load_cnt; l += kWarps) {
-        const int4 ld4 = ps.loads[tile.load_beg + l];
-        warp_load_window_v(sm + (size_t)ld4.y * L, in + (size_t)ld4.x * ld, wrap_any(s0 + ld4.z, H), S + ld4.w, H,
-                           lane);
+    if (sizeof(Acc) == 4 && ps.pair_loads) {
+        for (int l = warp; l < tile.load_cnt; l += 2 * kWarps) {
+            const int4 w0 = ps.loads[tile.load_beg + l];
+            const bool two = l + kWarps < tile.load_cnt;
+            const int4 w1 = two ? ps.loads[tile.load_beg + l + kWarps] : w0;
+            warp_load_window_pair(sm + (size_t)w0.y * L, in + (size_t)w0.x * ld, wrap_any(s0 + w0.z, H), S + w0.w,
+                                  two ? sm + (size_t)w1.y * L : nullptr, in + (size_t)w1.x * ld,
+                                  wrap_any(s0 + w1.z, H), S + w1.w, H, lane);
+        }
+    } else {
+        for (int l = warp; l < tile.load_cnt; l += kWarps) {
+            const int4 ld4 = ps.loads[tile.load_beg + l];
+            warp_load_window_v(sm + (size_t)ld4.y * L, in + (size_t)ld4.x * ld, wrap_any(s0 + ld4.z, H), S + ld4.w,
+                               H, lane);
+        }
     }
     // 2. merge levels
+    const uint32_t sbase = smem_u32(sm);
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
-        run_step<Acc, kWarps>(sm, L, sops, ps.step_offs[tile.step_beg + k] - op0,
-                              ps.step_offs[tile.step_beg + k + 1] - op0, S, warp, lane);
+        const int ob = ps.step_offs[tile.step_beg + k] - op0, oe = ps.step_offs[tile.step_beg + k + 1] - op0;
+        if constexpr (sizeof(Acc) == 4)
+            run_step_baked<Acc, kWarps>(sbase, sbops, ob, oe, warp, lane);
+        else
+            run_step<Acc, kWarps>(sm, L, sops, ob, oe, S, warp, lane);
     }
     __syncthreads();
     // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)

@@ -47,12 +47,14 @@ struct PassDev {
     const int4* loads;  // gcol, slot, off, ext
     const int* step_offs;
     const PassOpDev* ops;
+    const int4* bops;    // ops baked for 4-byte accumulators: shared byte offsets {dst, a, b|M, rows}
     const int2* stores;  // slot, gcol
     int ntiles;
     int S;       // rows per row tile
     int L;       // smem row capacity of a slot (>= S + max_ext, odd)
     int max_slots;
     int max_tile_ops;  // most merge ops in one tile (staged in shared memory)
+    int pair_loads;    // load two windows per warp at once (FHT_K2_PAIR_LOADS)
 };
 
 struct GroupLaunch {
