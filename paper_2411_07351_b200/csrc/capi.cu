@@ -114,6 +114,7 @@ struct fht_plan_s {
     int w = 0, h = 0, strategy = 1, in = 0, acc = 1, out = 1, mask = 15, batch = 1, layout = 0, device = 0;
     std::vector<std::unique_ptr<Group>> groups;
     int chunk = 1;
+    int num_sms = 148;
     size_t ws_bytes = 0;
     int launches = 0;
     uint64_t additions = 0;
@@ -259,7 +260,6 @@ void upload(Group& g) {
         d.bops = reinterpret_cast<const int4*>(base + o.bops);
         d.S = g.pass_S[i];
         d.L = g.pass_L[i];
-        d.pair_loads = env_int("FHT_K2_PAIR_LOADS", 0, 0, 1);
         d.ntiles = static_cast<int>(sp.passes[i].tiles.size());
         d.max_slots = sp.passes[i].max_slots;
         d.max_tile_ops = 0;
@@ -303,6 +303,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     DeviceGuard dg(device);
 
     auto p = std::make_unique<fht_plan_s>();
+    cuda_check(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
     p->w = w, p->h = h, p->strategy = strategy, p->in = in, p->acc = acc, p->out = out, p->mask = mask;
     p->batch = batch, p->layout = layout, p->device = device;
     const int bw = block_width_default();

@@ -13,6 +13,7 @@
 // is bound by HBM (or L2) bandwidth.  See DESIGN.md for the roofline model.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -291,36 +292,6 @@ __device__ __forceinline__ void run_step_baked(uint32_t base, const int4* __rest
             default: rows_op<3, Acc>(d, a, bb, n, lane); break;
         }
     }
-}
-
-// Two K2 windows per warp at once (4-byte types): the aligned, pre-wrap part
-// of each with up to 6 16-byte loads in flight per lane, then the remainder
-// (after the wrap point) with unrolled scalar loads.
-template <class Acc>
-__device__ __forceinline__ void warp_load_window_pair(Acc* d0, const Acc* __restrict__ c0, int st0, int n0, Acc* d1,
-                                                      const Acc* __restrict__ c1, int st1, int n1, int H,
-                                                      int lane) {
-    const int run0 = (st0 & 3) ? 0 : (min(n0, H - st0) & ~3);
-    const int run1 = (d1 && !(st1 & 3)) ? (min(n1, H - st1) & ~3) : 0;
-    const int4* __restrict__ s0p = reinterpret_cast<const int4*>(c0 + st0);
-    const int4* __restrict__ s1p = reinterpret_cast<const int4*>(c1 + (d1 ? st1 : 0));
-    for (int k0 = 0; k0 < max(run0, run1) / 4; k0 += 64) {
-        int4 v0[2], v1[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int k = k0 + lane + 32 * c;
-            if (4 * k < run0) v0[c] = s0p[k];
-            if (4 * k < run1) v1[c] = s1p[k];
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int k = k0 + lane + 32 * c;
-            if (4 * k < run0) sts4(d0 + 4 * k, v0[c]);
-            if (4 * k < run1) sts4(d1 + 4 * k, v1[c]);
-        }
-    }
-    if (run0 < n0) warp_load_window(d0 + run0, c0, wrap_any(st0 + run0, H), n0 - run0, H, lane);
-    if (d1 && run1 < n1) warp_load_window(d1 + run1, c1, wrap_any(st1 + run1, H), n1 - run1, H, lane);
 }
 
 // Column store smem -> global, rows [0, n): 16-byte stores when the global
@@ -665,6 +636,32 @@ size_t k1_by32_smem_bytes() { return (2 * kBYW * kBYSR + 16) * 4; }
 // reference layout hough[s*W + t] (transform.cpp:80-83).
 constexpr int kThreads2 = 512;
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Issue the window copies of one K2 tile (all warps; warp per window).
+template <class Acc>
+__device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileDev& tile, const Acc* __restrict__ in,
+                                              uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
+                                              int lane) {
+    for (int l = warp; l < tile.load_cnt; l += kThreads2 / 32) {
+        const int4 w = ps.loads[tile.load_beg + l];
+        const Acc* col = in + (size_t)w.x * ld;
+        const uint32_t d = stage + static_cast<uint32_t>(w.y) * L * 4u;
+        const int start = wrap_any(s0 + w.z, H), n = S + w.w;
+        const int run = (start & 3) ? 0 : (min(n, H - start) & ~3);
+        for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
+        for (int i = run + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(start + i, H));
+    }
+}
+
+
 template <class Acc, class Out>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
@@ -690,15 +687,12 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
             reinterpret_cast<int4*>(sops)[k] = reinterpret_cast<const int4*>(ps.ops + op0)[k];
     }
     // 1. windows of the input columns
-    if (sizeof(Acc) == 4 && ps.pair_loads) {
-        for (int l = warp; l < tile.load_cnt; l += 2 * kWarps) {
-            const int4 w0 = ps.loads[tile.load_beg + l];
-            const bool two = l + kWarps < tile.load_cnt;
-            const int4 w1 = two ? ps.loads[tile.load_beg + l + kWarps] : w0;
-            warp_load_window_pair(sm + (size_t)w0.y * L, in + (size_t)w0.x * ld, wrap_any(s0 + w0.z, H), S + w0.w,
-                                  two ? sm + (size_t)w1.y * L : nullptr, in + (size_t)w1.x * ld,
-                                  wrap_any(s0 + w1.z, H), S + w1.w, H, lane);
-        }
+    if constexpr (sizeof(Acc) == 4) {
+        // cp.async: every window copy of the tile in flight at once, no
+        // register staging (16-byte copies before the wrap point, 4-byte after)
+        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane);
+        cp_async_commit();
+        cp_async_wait0();
     } else {
         for (int l = warp; l < tile.load_cnt; l += kWarps) {
             const int4 ld4 = ps.loads[tile.load_beg + l];

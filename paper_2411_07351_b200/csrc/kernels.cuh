@@ -54,7 +54,6 @@ struct PassDev {
     int L;       // smem row capacity of a slot (>= S + max_ext, odd)
     int max_slots;
     int max_tile_ops;  // most merge ops in one tile (staged in shared memory)
-    int pair_loads;    // load two windows per warp at once (FHT_K2_PAIR_LOADS)
 };
 
 struct GroupLaunch {
