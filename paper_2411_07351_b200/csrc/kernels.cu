@@ -645,19 +645,31 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Issue the window copies of one K2 tile (all warps; warp per window).
+// Issue the window copies of one K2 tile (all warps; warp per window).  The
+// warp's window records are fetched with one load per lane up front and
+// broadcast with shuffles, so no descriptor load sits on the issue path.
 template <class Acc>
 __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileDev& tile, const Acc* __restrict__ in,
                                               uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
                                               int lane) {
-    for (int l = warp; l < tile.load_cnt; l += kThreads2 / 32) {
-        const int4 w = ps.loads[tile.load_beg + l];
-        const Acc* col = in + (size_t)w.x * ld;
-        const uint32_t d = stage + static_cast<uint32_t>(w.y) * L * 4u;
-        const int start = wrap_any(s0 + w.z, H), n = S + w.w;
-        const int run = (start & 3) ? 0 : (min(n, H - start) & ~3);
-        for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
-        for (int i = run + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(start + i, H));
+    constexpr int kW = kThreads2 / 32;
+    for (int base = 0; base < tile.load_cnt; base += 32 * kW) {
+        const int mine = base + warp + kW * lane;
+        const int4 rec = mine < tile.load_cnt ? ps.loads[tile.load_beg + mine] : make_int4(0, 0, 0, 0);
+        const int cnt = min(32, (tile.load_cnt - base - warp + kW - 1) / kW);
+        for (int j = 0; j < cnt; ++j) {
+            int4 w;
+            w.x = __shfl_sync(0xffffffffu, rec.x, j);
+            w.y = __shfl_sync(0xffffffffu, rec.y, j);
+            w.z = __shfl_sync(0xffffffffu, rec.z, j);
+            w.w = __shfl_sync(0xffffffffu, rec.w, j);
+            const Acc* col = in + (size_t)w.x * ld;
+            const uint32_t d = stage + static_cast<uint32_t>(w.y) * L * 4u;
+            const int start = wrap_any(s0 + w.z, H), n = S + w.w;
+            const int run = (start & 3) ? 0 : (min(n, H - start) & ~3);
+            for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
+            for (int i = run + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(start + i, H));
+        }
     }
 }
 
@@ -679,6 +691,8 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     // 0. stage the tile's merge ops in shared memory (after the slots)
     PassOpDev* sops = reinterpret_cast<PassOpDev*>(sm + (size_t)ps.max_slots * L + 16);
     int4* sbops = reinterpret_cast<int4*>(sops);
+    int* ssteps = reinterpret_cast<int*>(sops + ps.max_tile_ops);  // the tile's step offsets (after the ops)
+    if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid];
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
     if constexpr (sizeof(Acc) == 4) {
         for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
@@ -704,7 +718,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     const uint32_t sbase = smem_u32(sm);
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
-        const int ob = ps.step_offs[tile.step_beg + k] - op0, oe = ps.step_offs[tile.step_beg + k + 1] - op0;
+        const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
         if constexpr (sizeof(Acc) == 4)
             run_step_baked<Acc, kWarps>(sbase, sbops, ob, oe, warp, lane);
         else
@@ -716,9 +730,14 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     if (!final_pass) {
         Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
         const bool al = ((ld | s0) & 3) == 0;
-        for (int c = warp; c < tile.store_cnt; c += kWarps) {
-            const int2 st = ps.stores[tile.store_beg + c];
-            warp_store_col<Acc, Acc>(o + (size_t)st.y * ld + s0, sm + (size_t)st.x * L, rows, al, lane);
+        for (int cb = 0; cb < tile.store_cnt; cb += 32 * kWarps) {
+            const int mine = cb + warp + kWarps * lane;
+            const int2 rec = mine < tile.store_cnt ? ps.stores[tile.store_beg + mine] : make_int2(0, 0);
+            const int cnt = min(32, (tile.store_cnt - cb - warp + kWarps - 1) / kWarps);
+            for (int j = 0; j < cnt; ++j) {
+                const int sl = __shfl_sync(0xffffffffu, rec.x, j), gc = __shfl_sync(0xffffffffu, rec.y, j);
+                warp_store_col<Acc, Acc>(o + (size_t)gc * ld + s0, sm + (size_t)sl * L, rows, al, lane);
+            }
         }
     } else {
         const int nq = qs.n;
@@ -843,8 +862,9 @@ size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_
 
 size_t k2_smem_bytes(int acc_dtype, int max_slots, int L, int max_tile_ops) {
     const size_t esz = acc_dtype == kI64 ? 8 : 4;
-    // slots, +16 elements of vector-merge read slack, then the staged ops
-    return (static_cast<size_t>(max_slots) * L + 16) * esz + static_cast<size_t>(max_tile_ops) * sizeof(PassOpDev);
+    // slots, +16 elements of vector-merge read slack, the staged ops, the step offsets
+    return (static_cast<size_t>(max_slots) * L + 16) * esz + static_cast<size_t>(max_tile_ops) * sizeof(PassOpDev) +
+           64 * sizeof(int);
 }
 
 int launch_group(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* ctx) {
