@@ -136,6 +136,23 @@ int fht_fht2d_quadrants_i64(const int64_t* img, int width, int height, int strat
                             int64_t* horiz_neg, int64_t* vert_pos, int64_t* vert_neg,
                             uint64_t* total_additions);
 
+/* Structure-free validation path (the reference's oracle, oracle.cpp:9-25):
+ * J(t, s) = sum_x I(x, (pat_t(x) + s) mod h) by direct Theta(w^2 h)
+ * summation on the device with Algorithm-2 patterns (pattern.cpp:10-30),
+ * int64 accumulation, reference layout.  For checking the fast path at sizes
+ * where a CPU oracle is infeasible.
+ *   fht_slow_hough_device: integer image on the device (dtype FHT_U8 / FHT_I32
+ *     / FHT_I64), quadrant code 0..3 (QuadrantSet order), int64 output on the
+ *     device; stream ordered.
+ *   fht_slow_hough_i64 <-> fht::slow_hough (oracle.hpp:17), host buffers. */
+int fht_slow_hough_device(const void* d_img, int in_dtype, int width, int height, int strategy, int quadrant,
+                          int64_t* d_hough, void* stream);
+int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, int64_t* hough);
+
+/* Algorithm 2: the slope-t generating pattern of width n (n values)
+ * <-> fht::fht2d_pattern (pattern.hpp:20, pattern.cpp:24-30). */
+int fht_fht2d_pattern(int n, int t, int strategy, int* values);
+
 /* Host helpers, identical to the reference's integer rules. */
 int fht_split_width(int w, int strategy, int* w0, int* w1);                 /* split.hpp:46-48 */
 int fht_round_half_up_ratio(int64_t num, int64_t den, int64_t* result);     /* split.hpp:53-57 */

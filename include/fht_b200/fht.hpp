@@ -16,6 +16,8 @@
 //                                        transform.hpp:12-40
 //   flip_horizontal, transpose, QuadrantSet, fht2d_quadrants
 //                                        quadrants.hpp:10-33
+//   Pattern, fht2d_pattern, pattern_set  pattern.hpp:12-24
+//   slow_hough, count_additions_tree     oracle.hpp:15-22
 // fht2d / fht2d_counted / fht2d_quadrants run on the current CUDA device;
 // the overflow budget is checked there (std::overflow_error as in
 // transform.cpp:24-26).  Plan is the batched, device-resident interface.
@@ -186,6 +188,46 @@ inline QuadrantSet fht2d_quadrants(const Image& img, SplitStrategy strategy,
                                      &adds));
     if (total_additions) *total_additions = adds;
     return q;
+}
+
+// ------------------------------------------------------ patterns / oracle
+/// pattern.hpp:12-17
+struct Pattern {
+    int n = 0;
+    int t = 0;
+    std::vector<int> values;
+};
+
+/// Algorithm 2 (pattern.cpp:24-30).
+inline Pattern fht2d_pattern(int n, int t, SplitStrategy strategy) {
+    Pattern p{n, t, std::vector<int>(n > 0 ? static_cast<std::size_t>(n) : 0)};
+    throw_on(fht_fht2d_pattern(n, t, strategy_code(strategy), p.values.data()));
+    return p;
+}
+
+/// pattern.cpp:32-38
+inline std::vector<Pattern> pattern_set(int n, SplitStrategy strategy) {
+    if (n < 1) throw std::invalid_argument("pattern_set: width must be positive");
+    std::vector<Pattern> set;
+    set.reserve(static_cast<std::size_t>(n));
+    for (int t = 0; t < n; ++t) set.push_back(fht2d_pattern(n, t, strategy));
+    return set;
+}
+
+/// oracle.cpp:9-25: direct summation along every shifted pattern (on the GPU).
+inline HoughImage slow_hough(const Image& img, SplitStrategy strategy) {
+    if (img.empty()) throw std::invalid_argument("slow_hough: image is empty");
+    HoughImage out(img.width(), img.height());
+    throw_on(fht_slow_hough_i64(img.data().data(), img.width(), img.height(), strategy_code(strategy),
+                                out.data().data()));
+    return out;
+}
+
+/// oracle.cpp:27-33
+inline std::uint64_t count_additions_tree(int w, int h, SplitStrategy strategy) {
+    std::uint64_t r = 0;
+    throw_on(fht_count_additions_tree(w, h, strategy_code(strategy), &r));
+    return r;
 }
 
 // --------------------------------------------------------- batched plans

@@ -40,6 +40,9 @@ SIGNATURES = {
     "fht_check_budget": (_i, [_vp, _i, _i64, _i, _pi, _vp]),
     "fht_fht2d_counted_i64": (_i, [_pi64, _i, _i, _i, _pi64, _pu64]),
     "fht_fht2d_quadrants_i64": (_i, [_pi64, _i, _i, _i, _pi64, _pi64, _pi64, _pi64, _pu64]),
+    "fht_slow_hough_device": (_i, [_vp, _i, _i, _i, _i, _i, _pi64, _vp]),
+    "fht_slow_hough_i64": (_i, [_pi64, _i, _i, _i, _pi64]),
+    "fht_fht2d_pattern": (_i, [_i, _i, _i, _pi]),
     "fht_split_width": (_i, [_i, _i, _pi, _pi]),
     "fht_round_half_up_ratio": (_i, [_i64, _i64, _pi64]),
     "fht_count_additions_tree": (_i, [_i, _i, _i, _pu64]),

@@ -17,6 +17,7 @@
 #include "../../include/fht_b200.h"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "slow.cuh"
 
 using fhtb::GroupLaunch;
 using fhtb::QuadSet;
@@ -699,6 +700,68 @@ int fht_fht2d_quadrants_i64(const int64_t* img, int width, int height, int strat
     return guarded([&] {
         int64_t* outs[4] = {horiz_pos, horiz_neg, vert_pos, vert_neg};
         run_i64(img, width, height, strategy, FHT_ALL_QUADRANTS, outs, total_additions);
+    });
+}
+
+int fht_fht2d_pattern(int n, int t, int strategy, int* values) {
+    return guarded([&] {
+        if (!values) throw std::invalid_argument("fht2d_pattern: null output");
+        fhtb::build_pattern(n, t, strategy, values);
+    });
+}
+
+int fht_slow_hough_device(const void* d_img, int in_dtype, int width, int height, int strategy, int quadrant,
+                          int64_t* d_hough, void* stream) {
+    return guarded([&] {
+        if (!d_img || !d_hough) throw std::invalid_argument("slow_hough: null pointer");
+        if (width < 1 || height < 1) throw std::invalid_argument("slow_hough: image is empty");
+        if (in_dtype != FHT_U8 && in_dtype != FHT_I32 && in_dtype != FHT_I64)
+            throw std::invalid_argument("slow_hough: integer images only");
+        if (quadrant < 0 || quadrant > 3) throw std::invalid_argument("slow_hough: quadrant must be 0..3");
+        const int W = quadrant < 2 ? width : height, H = quadrant < 2 ? height : width;
+        std::vector<int> pat(static_cast<size_t>(W) * W);
+        for (int t = 0; t < W; ++t) fhtb::build_pattern(W, t, strategy, pat.data() + static_cast<size_t>(t) * W);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int* d_pat = nullptr;
+        long long* d_cols = nullptr;
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_pat), pat.size() * sizeof(int), st), "cudaMallocAsync");
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_cols), static_cast<size_t>(W) * H * 8, st), "cudaMallocAsync");
+        cuda_check(cudaMemcpyAsync(d_pat, pat.data(), pat.size() * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        fhtb::launch_slow_hough(d_img, in_dtype, width, height, quadrant, d_pat, W, H, d_cols,
+                                reinterpret_cast<long long*>(d_hough), st);
+        cuda_check(cudaGetLastError(), "slow_hough launch");
+        cuda_check(cudaFreeAsync(d_pat, st), "cudaFreeAsync");
+        cuda_check(cudaFreeAsync(d_cols, st), "cudaFreeAsync");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // the host pattern table goes out of scope
+    });
+}
+
+int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, int64_t* hough) {
+    return guarded([&] {
+        if (!img || width < 1 || height < 1) throw std::invalid_argument("slow_hough: image is empty");
+        cudaStream_t st = cudaStreamPerThread;
+        const size_t cells = static_cast<size_t>(width) * height;
+        void* d_in = nullptr;
+        void* d_out = nullptr;
+        cuda_check(cudaMallocAsync(&d_in, cells * 8, st), "cudaMallocAsync");
+        cuda_check(cudaMallocAsync(&d_out, cells * 8, st), "cudaMallocAsync");
+        try {
+            cuda_check(cudaMemcpyAsync(d_in, img, cells * 8, cudaMemcpyHostToDevice, st), "H2D");
+            check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), width, nullptr, st);  // oracle.cpp:11
+            const int rc = fht_slow_hough_device(d_in, FHT_I64, width, height, strategy, 0,
+                                                 static_cast<int64_t*>(d_out), st);
+            if (rc != FHT_OK) throw FhtError(rc, g_last_error);
+            cuda_check(cudaMemcpyAsync(hough, d_out, cells * 8, cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        } catch (...) {
+            cudaFreeAsync(d_in, st);
+            cudaFreeAsync(d_out, st);
+            cudaStreamSynchronize(st);
+            throw;
+        }
+        cudaFreeAsync(d_in, st);
+        cudaFreeAsync(d_out, st);
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     });
 }
 

@@ -40,6 +40,31 @@ uint64_t count_additions_tree(int w, int h, int strategy) {
 
 namespace {
 
+// pattern.cpp:10-20: split, rescale the slope to both parts (round half up),
+// recurse, lift the right part by t - t1.
+void pattern_values(int* out, int n, int t, int lift, int strategy) {
+    if (n == 1) {
+        out[0] = lift;
+        return;
+    }
+    const auto [n0, n1] = split_width(n, strategy);
+    const int t0 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (n0 - 1), n - 1));
+    const int t1 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(t) * (n1 - 1), n - 1));
+    pattern_values(out, n0, t0, lift, strategy);
+    pattern_values(out + n0, n1, t1, lift + (t - t1), strategy);
+}
+
+}  // namespace
+
+void build_pattern(int n, int t, int strategy, int* values) {
+    if (n < 1) throw std::invalid_argument("fht2d_pattern: width must be positive");
+    if (t < 0 || t >= n) throw std::invalid_argument("fht2d_pattern: slope must lie in [0, n)");
+    if (strategy != kSimple && strategy != kTweaked) throw std::invalid_argument("unknown split strategy");
+    pattern_values(values, n, t, 0, strategy);
+}
+
+namespace {
+
 struct Node {
     int x0, w, depth;
     int child[2];

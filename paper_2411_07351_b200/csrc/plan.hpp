@@ -110,3 +110,8 @@ struct SubPlan {
 };
 
 }  // namespace fhtb
+
+namespace fhtb {
+// pattern.cpp:10-30 (Algorithm 2): the slope-t generating pattern of width n.
+void build_pattern(int n, int t, int strategy, int* values);
+}  // namespace fhtb

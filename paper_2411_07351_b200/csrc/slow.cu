@@ -1,0 +1,67 @@
+// slow.cu -- structure-free direct summation on the device, the GPU form of
+// the reference's validation oracle slow_hough (oracle.cpp:9-25):
+//     J(t, s) = sum_x I(x, (pat_t(x) + s) mod h)
+// with pat_t the Algorithm-2 pattern (pattern.cpp:10-30) built on the host.
+// Theta(w^2 h) work: it exists to check the fast path at sizes where the CPU
+// oracle is infeasible, not for speed.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "slow.cuh"
+
+namespace fhtb {
+namespace {
+
+// The working column-major copy of one quadrant: cols[x*h + y].
+template <class In>
+__global__ void k_columns(const In* __restrict__ img, int img_w, int img_h, int q, long long* __restrict__ cols,
+                          int W, int H) {
+    const long long n = (long long)W * H;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int x = static_cast<int>(k / H), y = static_cast<int>(k % H);
+        long long v;
+        switch (q) {
+            case 0: v = static_cast<long long>(img[(size_t)y * img_w + x]); break;
+            case 1: v = static_cast<long long>(img[(size_t)y * img_w + (img_w - 1 - x)]); break;
+            case 2: v = static_cast<long long>(img[(size_t)x * img_w + y]); break;
+            default: v = static_cast<long long>(img[(size_t)(img_h - 1 - x) * img_w + y]); break;
+        }
+        cols[k] = v;
+    }
+}
+
+// One thread per (t, s); lanes over consecutive s read consecutive rows of
+// each column (coalesced); the pattern row is warp-uniform.
+__global__ void k_slow(const long long* __restrict__ cols, const int* __restrict__ pat, int W, int H,
+                       long long* __restrict__ out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    if (s >= H) return;
+    const int* __restrict__ p = pat + (size_t)t * W;
+    long long acc = 0;
+    for (int x = 0; x < W; ++x) {
+        int y = (p[x] % H) + s;
+        if (y >= H) y -= H;
+        acc += cols[(size_t)x * H + y];
+    }
+    out[(size_t)s * W + t] = acc;  // reference layout hough[s*W + t]
+}
+
+}  // namespace
+
+void launch_slow_hough(const void* img, int in_dtype, int img_w, int img_h, int q, const int* d_pat, int W, int H,
+                       long long* d_cols, long long* d_out, cudaStream_t st) {
+    const int blocks = 148 * 8;
+    if (in_dtype == 0)
+        k_columns<uint8_t><<<blocks, 256, 0, st>>>(static_cast<const uint8_t*>(img), img_w, img_h, q, d_cols, W, H);
+    else if (in_dtype == 1)
+        k_columns<int32_t><<<blocks, 256, 0, st>>>(static_cast<const int32_t*>(img), img_w, img_h, q, d_cols, W, H);
+    else
+        k_columns<long long><<<blocks, 256, 0, st>>>(static_cast<const long long*>(img), img_w, img_h, q, d_cols, W,
+                                                     H);
+    dim3 g((H + 255) / 256, W);
+    k_slow<<<g, 256, 0, st>>>(d_cols, d_pat, W, H, d_out);
+}
+
+}  // namespace fhtb

@@ -177,6 +177,60 @@ def fht2d_quadrants(img, strategy=SplitStrategy.Tweaked, total_additions: list |
     return QuadrantSet(*outs)
 
 
+@dataclass
+class Pattern:
+    """pattern.hpp:12-17"""
+    n: int
+    t: int
+    values: list
+
+
+def fht2d_pattern(n: int, t: int, strategy=SplitStrategy.Tweaked) -> Pattern:
+    """fht::fht2d_pattern (pattern.cpp:24-30, Algorithm 2)."""
+    v = (ctypes.c_int * max(n, 1))()
+    check(lib().fht_fht2d_pattern(n, t, _strategy(strategy), v))
+    return Pattern(n, t, list(v)[:n])
+
+
+def pattern_set(n: int, strategy=SplitStrategy.Tweaked) -> list:
+    """fht::pattern_set (pattern.cpp:32-38)."""
+    if n < 1:
+        raise InvalidArgument("pattern_set: width must be positive")
+    return [fht2d_pattern(n, t, strategy) for t in range(n)]
+
+
+def slow_hough(img, strategy=SplitStrategy.Tweaked) -> np.ndarray:
+    """fht::slow_hough (oracle.cpp:9-25): direct summation along every shifted
+    pattern, on the GPU (int64, bit-exact for integer images)."""
+    a = _as_image(img)
+    h, w = a.shape
+    out = np.empty((h, w), dtype=np.int64)
+    p = ctypes.POINTER(ctypes.c_int64)
+    check(lib().fht_slow_hough_i64(a.ctypes.data_as(p), w, h, _strategy(strategy), out.ctypes.data_as(p)))
+    return out
+
+
+def slow_hough_device(x, quadrant: str = "horiz_pos", strategy=SplitStrategy.Tweaked, stream=None):
+    """Device slow_hough of one quadrant of an integer CUDA image tensor (h, w);
+    returns an int64 CUDA tensor in the reference layout."""
+    import torch
+
+    if x.dim() != 2 or not x.is_cuda or not x.is_contiguous():
+        raise InvalidArgument("expected a contiguous 2-D CUDA tensor")
+    code = {torch.uint8: FHT_U8, torch.int32: FHT_I32, torch.int64: FHT_I64}.get(x.dtype)
+    if code is None:
+        raise InvalidArgument("slow_hough_device: integer images only")
+    h, w = x.shape
+    q = QUADRANTS.index(quadrant)
+    shape = (h, w) if q < 2 else (w, h)
+    out = torch.empty(shape, dtype=torch.int64, device=x.device)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    check(lib().fht_slow_hough_device(ctypes.c_void_p(x.data_ptr()), code, w, h, _strategy(strategy), q,
+                                      ctypes.cast(ctypes.c_void_p(out.data_ptr()), ctypes.POINTER(ctypes.c_int64)),
+                                      ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
 def check_overflow_budget(img) -> None:
     """fht::check_overflow_budget (transform.cpp:16-27), evaluated on the device."""
     import torch
@@ -304,6 +358,7 @@ class Plan:
 
 
 __all__ = ["SplitStrategy", "strategy_from_string", "split_width", "split_simple", "split_tweaked",
-           "round_half_up_ratio", "count_additions_tree", "CountedTransform", "QuadrantSet", "fht2d",
+           "round_half_up_ratio", "count_additions_tree", "CountedTransform", "QuadrantSet", "fht2d", "Pattern",
+           "fht2d_pattern", "pattern_set", "slow_hough", "slow_hough_device",
            "fht2d_counted", "fht2d_quadrants", "check_overflow_budget", "Plan", "QUADRANTS", "InvalidArgument",
            "OverflowBudget", "_lib"]

@@ -95,6 +95,15 @@ int main() {
         fht::QuadrantSet q = fht::fht2d_quadrants(img, fht::SplitStrategy::Tweaked);
         for (size_t i = 0; i < img.data().size(); ++i) CHECK(out[2][64 * 48 + i] == q.vert_pos.data()[i]);
     }
+    // patterns and the structure-free oracle (pattern.cpp, oracle.cpp)
+    CHECK(fht::fht2d_pattern(4, 1, fht::SplitStrategy::Tweaked).values == std::vector<int>({0, 0, 1, 1}));
+    CHECK(fht::pattern_set(4, fht::SplitStrategy::Tweaked)[2].values == std::vector<int>({0, 1, 1, 2}));
+    CHECK(fht::count_additions_tree(17, 17, fht::SplitStrategy::Tweaked) == 1377);
+    {
+        fht::Image img(45, 31);
+        for (auto& v : img.data()) v = dist(rng);
+        CHECK(fht::slow_hough(img, fht::SplitStrategy::Simple) == fht::fht2d(img, fht::SplitStrategy::Simple));
+    }
     std::printf("%s (%d failures)\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }
