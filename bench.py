@@ -217,7 +217,20 @@ def run_ours(args):
     c = workloads.CONFIGS[args.config]
     strategy = 0 if args.strategy == "simple" else 1
 
-    if c.batch == 1 and ws > 1:
+    root_split = None
+    if c.batch == 1 and ws > len(c.quadrants):
+        # one large image on more ranks than quadrants: two ranks per quadrant,
+        # each computes one child subtree of the root, they swap half of their
+        # child columns (one NCCL send/recv pair) and each merges half the root
+        pair = rank // 2
+        my_q = [c.quadrants[pair]] if pair < len(c.quadrants) else []
+        root_split = (rank % 2, rank ^ 1) if my_q and (rank ^ 1) < ws else None
+        if my_q and root_split is None:
+            my_q = list(my_q)  # unpaired last rank: whole quadrant alone
+        imgs = workloads.make_images(args.config, 1)
+        scaling = "strong"
+        sums_per_step = workloads.nominal_sums(args.config)
+    elif c.batch == 1 and ws > 1:
         # one large image: split its quadrants over the ranks (strong scaling)
         my_q = shard.quadrant_shard(ws, rank, c.quadrants)
         imgs = workloads.make_images(args.config, 1)
@@ -244,8 +257,15 @@ def run_ours(args):
     for i, q in enumerate(fht.QUADRANTS):
         ptrs[i] = out[q].data_ptr() if q in out else None
 
+    if root_split is not None:
+        rs_backend = shard.GpuRootBackend(strategy, c.dtype, c.acc)
+
     def step():
         if my_q is None:
+            return
+        if root_split is not None:
+            shard.root_split_quadrant(x[0], my_q[0], strategy, side=root_split[0], backend=rs_backend,
+                                      peer=root_split[1])
             return
         check(lib().fht_execute(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
                                 ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
@@ -334,7 +354,7 @@ def run_ours(args):
 
     # e2e through the C-ABI host-buffer call (pinned host memory).
     e2e = None
-    if not args.no_e2e and my_q is not None:
+    if not args.no_e2e and my_q is not None and root_split is None:
         h_in = torch.from_numpy(imgs).pin_memory()
         h_out = {q: torch.empty(out[q].shape, dtype=out[q].dtype).pin_memory() for q in out}
         optrs = [h_out[q].data_ptr() if q in h_out else None for q in fht.QUADRANTS]
@@ -369,7 +389,8 @@ def run_ours(args):
             "config": {"workload": args.config, "description": c.description, "n": c.n,
                        "images_per_gpu": c.batch, "quadrants": len(c.quadrants), "strategy": args.strategy,
                        "in_dtype": c.dtype, "acc_dtype": c.acc,
-                       "parallelism": (f"quadrant-split x{ws}" if scaling == "strong" else f"batch-shard x{ws}"),
+                       "parallelism": (("root-split x2 per quadrant" if ws > len(c.quadrants) else f"quadrant-split x{ws}")
+                                       if scaling == "strong" else f"batch-shard x{ws}"),
                        "l2": "flushed between timed steps (512 MiB write, untimed)"},
             "images_per_s": round((c.batch * ws if scaling == "weak" else 1) / (ms_per_step * 1e-3), 1),
             "hbm_gbs_step": round(step_gbs, 1),

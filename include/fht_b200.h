@@ -103,6 +103,25 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len);
 int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],
                 int64_t out_image_stride, void* d_workspace, void* stream);
 
+/* fht_execute on a pitched image view: row y of image i starts at
+ * d_in + i*in_image_stride + y*in_row_pitch elements (in_row_pitch >= width).
+ * Lets a plan run on a sub-image, e.g. one child subtree of the root in the
+ * multi-GPU root split. */
+int fht_execute_pitched(fht_plan_t plan, const void* d_in, int64_t in_row_pitch, int64_t in_image_stride,
+                        void* const d_out[4], int64_t out_image_stride, void* d_workspace, void* stream);
+
+/* The root level of a width-W, H-shift transform from its two children, each
+ * given as a slope-major column range (the FHT_LAYOUT_NATIVE output of a plan
+ * over that child's columns): left child slopes [left_first, ...) at d_left,
+ * right child slopes [right_first, ...) at d_right, column stride H.  Writes
+ * root slopes [t_begin, t_end) of d_out (reference layout hough[s*W + t] or
+ * native hough[t*H + s]):  OUT[t][s] = L[t0][s] + R[t1][(s + r) mod H]
+ * (transform.cpp:46-57).  Used by the multi-GPU root split, where each GPU
+ * owns one child and merges half the root.  Synchronises `stream`. */
+int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_dtype, int layout, const void* d_left,
+                   int left_first, const void* d_right, int right_first, int t_begin, int t_end, void* d_out,
+                   void* stream);
+
 /* fht_execute with a CUDA event recorded after every kernel launch on
  * `stream`; synchronises and returns each launch's duration (ms), kind
  * (1 = K1 generic blocks, 4 = K1P width-32 Brady-Yong blocks, 2 = K2 fused

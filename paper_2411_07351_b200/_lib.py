@@ -35,6 +35,8 @@ SIGNATURES = {
     "fht_plan_describe": (_i, [_vp, ctypes.c_char_p, ctypes.c_size_t]),
     "fht_execute": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp]),
     "fht_execute_host": (_i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
+    "fht_execute_pitched": (_i, [_vp, _vp, _i64, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp]),
+    "fht_merge_root": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp]),
     "fht_execute_profiled": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp, ctypes.POINTER(ctypes.c_float),
                                   _pi, ctypes.POINTER(ctypes.c_double), _i, _pi]),
     "fht_check_budget": (_i, [_vp, _i, _i64, _i, _pi, _vp]),

@@ -407,7 +407,9 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
 }
 
 void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_out[4], int64_t out_stride,
-             void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr) {
+             void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr, int64_t in_pitch = 0) {
+    if (in_pitch == 0) in_pitch = p->w;
+    if (in_pitch < p->w) throw std::invalid_argument("fht_execute: row pitch smaller than the image width");
     if (!d_in) throw std::invalid_argument("fht_execute: null input");
     for (int q = 0; q < 4; ++q)
         if ((p->mask & (1 << q)) && !d_out[q]) throw std::invalid_argument("fht_execute: null output for a selected quadrant");
@@ -422,6 +424,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.in_dtype = p->in;
             L.img_w = p->w;
             L.img_h = p->h;
+            L.img_pitch = in_pitch;
             L.img_stride = in_stride;
             L.img0 = img0;
             L.nimg = nimg;
@@ -674,6 +677,43 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
     });
     for (cudaEvent_t e : c.ev) cudaEventDestroy(e);
     return rc;
+}
+
+int fht_execute_pitched(fht_plan_t plan, const void* d_in, int64_t in_row_pitch, int64_t in_image_stride,
+                        void* const d_out[4], int64_t out_image_stride, void* d_workspace, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_out) throw std::invalid_argument("fht_execute_pitched: null argument");
+        execute(plan, d_in, in_image_stride, d_out, out_image_stride, d_workspace, static_cast<cudaStream_t>(stream),
+                nullptr, nullptr, in_row_pitch);
+    });
+}
+
+int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_dtype, int layout, const void* d_left,
+                   int left_first, const void* d_right, int right_first, int t_begin, int t_end, void* d_out,
+                   void* stream) {
+    return guarded([&] {
+        if (width < 2 || height < 1) throw std::invalid_argument("merge_root: the root must have width >= 2");
+        if (!d_left || !d_right || !d_out) throw std::invalid_argument("merge_root: null pointer");
+        if (t_begin < 0 || t_end > width || t_begin > t_end) throw std::invalid_argument("merge_root: bad slope range");
+        if (layout != FHT_LAYOUT_REFERENCE && layout != FHT_LAYOUT_NATIVE) throw std::invalid_argument("unknown layout");
+        const auto [w0, w1] = fhtb::split_width(width, strategy);
+        std::vector<int4> ops(static_cast<size_t>(width));
+        for (int t = 0; t < width; ++t) {  // transform.cpp:46-49
+            const int t0 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), width - 1));
+            const int t1 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), width - 1));
+            ops[static_cast<size_t>(t)] = make_int4(t, t0, t1, (t - t1) % height);
+        }
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int4* d_ops = nullptr;
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_ops), ops.size() * sizeof(int4), st), "cudaMallocAsync");
+        cuda_check(cudaMemcpyAsync(d_ops, ops.data(), ops.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "H2D");
+        const int rc = fhtb::launch_merge_root(d_ops, d_left, left_first, d_right, right_first, width, height, t_begin,
+                                               t_end, d_out, acc_dtype, out_dtype, layout, st);
+        cudaFreeAsync(d_ops, st);
+        if (rc < 0) throw std::invalid_argument("merge_root: unsupported (accumulator, output) dtype pair");
+        cuda_check(cudaGetLastError(), "merge_root launch");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // the host op table goes out of scope
+    });
 }
 
 int fht_execute_host(fht_plan_t plan, const void* h_in, void* const h_out[4], void* stream) {

@@ -34,18 +34,6 @@ __device__ __forceinline__ int wrap_any(int j, int H) {
     return j;
 }
 
-// Element (working column x, working row y) of quadrant q of a row-major image.
-template <class In>
-__device__ __forceinline__ In load_quadrant(const In* __restrict__ im, int q, int x, int y, int img_w,
-                                            int img_h) {
-    switch (q) {
-        case 0: return im[(size_t)y * img_w + x];
-        case 1: return im[(size_t)y * img_w + (img_w - 1 - x)];
-        case 2: return im[(size_t)x * img_w + y];
-        default: return im[(size_t)(img_h - 1 - x) * img_w + y];
-    }
-}
-
 constexpr int kU = 8;  // independent global loads in flight per lane
 
 // d[i] = col[(start + i) mod H] for i in [0, n), one warp, kU loads in flight per lane.
@@ -317,7 +305,8 @@ __device__ __forceinline__ size_t k1_ops_offset_dev(size_t esz, int max_width, i
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
 template <class In, class Acc, class Out>
 __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
-    const In* __restrict__ img, int img_w, int img_h, long long img_stride, int img0, QuadSet qs, int W, int H,
+    const In* __restrict__ img, int img_w, int img_h, long long img_pitch, long long img_stride, int img0, QuadSet qs,
+    int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
     const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, int max_width, int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out) {
@@ -360,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
             for (int u = 0; u < kUH; ++u) {
                 const int i = ib + u * kWarps;
                 if (i < R) {
-                    const In* __restrict__ rowp = im + (size_t)wrap_any(s0 + i, H) * img_w;
+                    const In* __restrict__ rowp = im + (size_t)wrap_any(s0 + i, H) * img_pitch;
                     if (lane < wb) v[u][0] = rowp[xa + dx * lane];
                     if (lane + 32 < wb) v[u][1] = rowp[xa + dx * (lane + 32)];
                 }
@@ -381,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
         // working column = image row (reversed rows for vert_neg): contiguous.
         for (int c = warp; c < wb; c += kWarps) {
             const int row = (q == 2) ? x0 + c : img_h - 1 - (x0 + c);
-            warp_load_window(lbuf + c * sr, im + (size_t)row * img_w, s0, R, H, lane);
+            warp_load_window(lbuf + c * sr, im + (size_t)row * img_pitch, s0, R, H, lane);
         }
     }
 
@@ -525,7 +514,7 @@ __device__ __forceinline__ void by_level12(Acc* sm, int S, int tid) {
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
 template <class In, class Acc, int V>
 __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
-                                                          long long img_stride, int img0, QuadSet qs, int W, int H,
+                                                          long long img_pitch, long long img_stride, int img0, QuadSet qs, int W, int H,
                                                           int ld, int S, const int* __restrict__ bx0,
                                                           Acc* __restrict__ ws, int nbuf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -551,7 +540,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
 #pragma unroll
         for (int k = 0; k < kRowsPerWarp; ++k) {
             const int i = warp + k * kWarpsBY;
-            if (i < R) v[k] = im[(size_t)wrap_any(s0 + i, H) * img_w + xx];
+            if (i < R) v[k] = im[(size_t)wrap_any(s0 + i, H) * img_pitch + xx];
         }
 #pragma unroll
         for (int k = 0; k < kRowsPerWarp; ++k) {
@@ -575,7 +564,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         for (int h = 0; h < 2; ++h) {
             const int c = warp + h * kWarpsBY;
             const int row = (q == 2) ? x0 + c : img_h - 1 - (x0 + c);
-            const In* __restrict__ rp = im + (size_t)row * img_w;
+            const In* __restrict__ rp = im + (size_t)row * img_pitch;
 #pragma unroll
             for (int k = 0; k < kRowsPerLane; ++k) {
                 const int i = lane + 32 * k;
@@ -784,6 +773,46 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     }
 }
 
+// ------------------------------------------------------------ root merge
+// The root level from its two children held as separate slope-major column
+// ranges (the multi-GPU root split): output slopes [t_beg,
+// t_end) of a width-W node, OUT[t][s] = L[t0][s] + R[t1][(s + r) mod H]
+// (transform.cpp:46-57), tiles of 32 slopes x 32 shifts transposed through
+// shared memory into the reference layout (or written slope-major).
+template <class Acc, class Out>
+__global__ void __launch_bounds__(256) k_merge_root(const int4* __restrict__ ops, const Acc* __restrict__ left,
+                                                     int left_first, const Acc* __restrict__ right, int right_first,
+                                                     int W, int H, int t_beg, int t_end, Out* __restrict__ out,
+                                                     int layout) {
+    __shared__ Acc tile[32][33];
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int t0 = t_beg + blockIdx.x * 32, s0 = blockIdx.y * 32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int tl = ty + 8 * j, t = t0 + tl, s = s0 + lane;
+        if (t < t_end && s < H) {
+            const int4 op = ops[t];  // (t, t0, t1, r)
+            int jb = s + op.w;
+            if (jb >= H) jb -= H;
+            tile[tl][lane] = left[(size_t)(op.y - left_first) * H + s] + right[(size_t)(op.z - right_first) * H + jb];
+        }
+    }
+    __syncthreads();
+    if (layout == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int sl = ty + 8 * j, s = s0 + sl, t = t0 + lane;
+            if (s < H && t < t_end) out[(size_t)s * W + t] = static_cast<Out>(tile[lane][sl]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int tl = ty + 8 * j, t = t0 + tl, s = s0 + lane;
+            if (t < t_end && s < H) out[(size_t)t * H + s] = static_cast<Out>(tile[tl][lane]);
+        }
+    }
+}
+
 // --------------------------------------------------------------- absmax
 template <class T>
 __global__ void k_absmax(const T* __restrict__ in, long long n, unsigned long long* __restrict__ out) {
@@ -815,7 +844,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
-            kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride,
+            kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
+                                              g.img_stride,
                                               g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
             ++launches;
             if (hook) hook(ctx, 4);
@@ -823,7 +853,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     }
     if (g.nblocks > 0) {
         dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
-        k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_stride, g.img0,
+        k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
+                                       g.img_stride, g.img0,
                                        g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs, g.k1_ops,
                                        g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out);
         ++launches;
@@ -888,6 +919,24 @@ int launch_group(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         if (in == kU8) return launch_typed<uint8_t, float, float>(g, st, hook, ctx);
     }
     return -1;
+}
+
+int launch_merge_root(const int4* d_ops, const void* left, int left_first, const void* right, int right_first,
+                      int W, int H, int t_beg, int t_end, void* out, int acc, int outd, int layout, cudaStream_t st) {
+    if (t_end <= t_beg) return 0;
+    dim3 g((t_end - t_beg + 31) / 32, (H + 31) / 32);
+    dim3 b(32, 8);
+#define FHT_MERGE(A, O)                                                                                        \
+    k_merge_root<A, O><<<g, b, 0, st>>>(d_ops, static_cast<const A*>(left), left_first,                       \
+                                        static_cast<const A*>(right), right_first, W, H, t_beg, t_end,          \
+                                        static_cast<O*>(out), layout)
+    if (acc == kI32 && outd == kI32) FHT_MERGE(int32_t, int32_t);
+    else if (acc == kI32 && outd == kI64) FHT_MERGE(int32_t, long long);
+    else if (acc == kI64 && outd == kI64) FHT_MERGE(long long, long long);
+    else if (acc == kF32 && outd == kF32) FHT_MERGE(float, float);
+    else return -1;
+#undef FHT_MERGE
+    return 1;
 }
 
 void launch_absmax(const void* d_in, int dtype, long long n, unsigned long long* d_max, cudaStream_t st) {

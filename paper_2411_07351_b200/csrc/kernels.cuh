@@ -61,6 +61,7 @@ struct GroupLaunch {
     const void* img;
     int in_dtype;
     int img_w, img_h;
+    long long img_pitch;  // elements between image rows (>= img_w)
     long long img_stride;
     int img0;      // first image of this chunk
     int nimg;      // images in this chunk
@@ -98,6 +99,12 @@ size_t k2_smem_bytes(int acc_dtype, int max_slots, int L, int max_tile_ops);
 // 3 = K2 writing the root.
 typedef void (*LaunchHook)(void* ctx, int kind);
 int launch_group(const GroupLaunch& g, cudaStream_t stream, LaunchHook hook = nullptr, void* ctx = nullptr);
+
+// Root merge of a width-W node from its children's slope-major column ranges
+// (left columns [left_first, ...), right columns [right_first, ...)), output
+// slopes [t_beg, t_end); d_ops[t] = (t, t0, t1, r).  Returns -1 on a bad type pair.
+int launch_merge_root(const int4* d_ops, const void* left, int left_first, const void* right, int right_first,
+                      int W, int H, int t_beg, int t_end, void* out, int acc, int outd, int layout, cudaStream_t st);
 
 // Device max |v| over n int32/int64 values into *d_max (must be zeroed).
 void launch_absmax(const void* d_in, int dtype, long long n, unsigned long long* d_max, cudaStream_t stream);

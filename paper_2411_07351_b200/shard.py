@@ -64,3 +64,151 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+# ----------------------------------------------------------- root split
+@dataclass(frozen=True)
+class RootSplit:
+    """Two GPUs share one quadrant of a large image (SURVEY §8e, config c5 on
+    8 GPUs): side 0 computes the root's left child subtree (working columns
+    [0, w0)), side 1 the right child ([w0, W)); they swap the child columns
+    the other side needs and each merges half of the root's slopes:
+    side 0 slopes [0, t_mid), side 1 [t_mid, W) (transform.cpp:46-57)."""
+    W: int
+    H: int
+    w0: int
+    w1: int
+    t_mid: int
+    right_for_0: tuple  # right-child slopes [lo, hi) side 1 sends to side 0
+    left_for_1: tuple   # left-child slopes [lo, hi) side 0 sends to side 1
+
+
+def root_split(W: int, H: int, strategy) -> RootSplit:
+    from .fht import round_half_up_ratio, split_width
+
+    if W < 2:
+        raise ValueError("root split needs width >= 2")
+    w0, w1 = split_width(W, strategy)
+    t_mid = W // 2
+
+    def t0(t):
+        return round_half_up_ratio(t * (w0 - 1), W - 1)
+
+    def t1(t):
+        return round_half_up_ratio(t * (w1 - 1), W - 1)
+
+    return RootSplit(W, H, w0, w1, t_mid, (t1(0), t1(t_mid - 1) + 1), (t0(t_mid), t0(W - 1) + 1))
+
+
+def child_view(img, quadrant: str, side: int, split: RootSplit):
+    """The sub-image whose `quadrant` transform is the root's child `side`
+    (a view: rows keep the parent's pitch).  Returns the 2-D view."""
+    h, w = img.shape
+    x0, cw = (0, split.w0) if side == 0 else (split.w0, split.w1)
+    if quadrant == "horiz_pos":
+        return img[:, x0:x0 + cw]
+    if quadrant == "horiz_neg":
+        return img[:, w - x0 - cw:w - x0]
+    if quadrant == "vert_pos":
+        return img[x0:x0 + cw, :]
+    if quadrant == "vert_neg":
+        return img[h - x0 - cw:h - x0, :]
+    raise ValueError(quadrant)
+
+
+class GpuRootBackend:
+    """Child transforms with a pitched plan (fht_execute_pitched, slope-major
+    output) and the root merge kernel (fht_merge_root)."""
+
+    def __init__(self, strategy, in_dtype: str, acc_dtype: str, out_dtype: str | None = None, layout="reference"):
+        self.strategy, self.in_dtype, self.acc_dtype = strategy, in_dtype, acc_dtype
+        self.out_dtype = out_dtype or acc_dtype
+        self.layout = layout
+        self._plans = {}
+
+    def child(self, view, quadrant: str, side: int = 0):
+        import ctypes
+
+        import torch
+
+        from . import fht
+        from ._lib import check, lib
+
+        h, w = view.shape
+        key = (w, h, quadrant, side, view.device.index or 0)  # per side: loopback keeps both children
+        if key not in self._plans:  # plans (tables, workspace, outputs) are built once per shape
+            plan = fht.Plan(w, h, self.strategy, in_dtype=self.in_dtype, acc_dtype=self.acc_dtype,
+                            quadrants=[quadrant], layout="native", device=view.device.index or 0)
+            self._plans[key] = (plan, plan.alloc_outputs(), plan.workspace())
+        plan, out, ws = self._plans[key]
+        ptrs = (ctypes.c_void_p * 4)()
+        ptrs[fht.QUADRANTS.index(quadrant)] = out[quadrant].data_ptr()
+        st = torch.cuda.current_stream(view.device)
+        check(lib().fht_execute_pitched(plan._h, ctypes.c_void_p(view.data_ptr()), view.stride(0), 0, ptrs, 0,
+                                        ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
+                                        ctypes.c_void_p(st.cuda_stream)))
+        return out[quadrant][0]  # (child width, H) slope-major
+
+    def merge(self, split: RootSplit, left, left_first, right, right_first, t_beg, t_end, out):
+        import ctypes
+
+        import torch
+
+        from . import fht
+        from ._lib import check, lib
+
+        st = torch.cuda.current_stream(out.device)
+        check(lib().fht_merge_root(split.W, split.H, fht._strategy(self.strategy), fht._dtype_code(self.acc_dtype),
+                                   fht._dtype_code(self.out_dtype), 0 if self.layout == "reference" else 1,
+                                   ctypes.c_void_p(left.data_ptr()), left_first, ctypes.c_void_p(right.data_ptr()),
+                                   right_first, t_beg, t_end, ctypes.c_void_p(out.data_ptr()),
+                                   ctypes.c_void_p(st.cuda_stream)))
+
+    def empty_out(self, split: RootSplit, like):
+        import torch
+
+        dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[self.out_dtype]
+        shape = (split.H, split.W) if self.layout == "reference" else (split.W, split.H)
+        return torch.zeros(shape, dtype=dt, device=like.device)
+
+
+def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: int | None = None, group=None):
+    """One side of the two-GPU root split of `quadrant` of `img` (the whole
+    image, resident on this rank).  `peer` is the other side's global rank
+    (None: both sides run in this process, `side` ignored -- used to test the
+    kernels on one GPU).  Returns this side's output buffer (full size, the
+    slopes this side merged filled in) and the split description."""
+    import torch
+    import torch.distributed as dist
+
+    horiz = quadrant.startswith("horiz")
+    h, w = img.shape
+    W, H = (w, h) if horiz else (h, w)
+    sp = root_split(W, H, strategy)
+    if peer is None:  # loopback: both children and both halves here
+        left = backend.child(child_view(img, quadrant, 0, sp), quadrant, 0)
+        right = backend.child(child_view(img, quadrant, 1, sp), quadrant, 1)
+        out = backend.empty_out(sp, left)
+        backend.merge(sp, left, 0, right, 0, 0, W, out)
+        return out, sp
+    mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side)
+    if side == 0:
+        lo, hi = sp.left_for_1
+        send = mine[lo:hi].contiguous()
+        rlo, rhi = sp.right_for_0
+        recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
+        ops = [dist.P2POp(dist.isend, send, peer, group), dist.P2POp(dist.irecv, recv, peer, group)]
+    else:
+        lo, hi = sp.right_for_0
+        send = mine[lo:hi].contiguous()
+        rlo, rhi = sp.left_for_1
+        recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
+        ops = [dist.P2POp(dist.irecv, recv, peer, group), dist.P2POp(dist.isend, send, peer, group)]
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    out = backend.empty_out(sp, mine)
+    if side == 0:
+        backend.merge(sp, mine, 0, recv, rlo, 0, sp.t_mid, out)
+    else:
+        backend.merge(sp, recv, rlo, mine, 0, sp.t_mid, W, out)
+    return out, sp

@@ -77,3 +77,61 @@ def test_gather_matches_single_process(tmp_path):
         q, _ = oracle.fht2d_quadrants(imgs[i], oracle.TWEAKED, dtype=np.int32)
         ref.append(np.stack([q["horiz_pos"], q["horiz_neg"]]))
     np.testing.assert_array_equal(np.load(out), np.stack(ref))
+
+
+# ------------------------------------------------------------ root split
+class _CpuRootBackend:
+    """The root split driven by the oracle on CPU tensors (no GPU here)."""
+
+    def __init__(self, strategy):
+        self.strategy = strategy
+
+    def child(self, view, quadrant, side=0):
+        import oracle
+
+        v = view.numpy()
+        q, _ = oracle.fht2d_quadrants(np.ascontiguousarray(v), self.strategy, dtype=np.int64)
+        return torch.from_numpy(np.ascontiguousarray(q[quadrant].T))  # slope-major (W_child, H)
+
+    def merge(self, sp, left, left_first, right, right_first, t_beg, t_end, out):
+        from paper_2411_07351_b200.fht import round_half_up_ratio
+
+        for t in range(t_beg, t_end):
+            t0 = round_half_up_ratio(t * (sp.w0 - 1), sp.W - 1)
+            t1 = round_half_up_ratio(t * (sp.w1 - 1), sp.W - 1)
+            r = (t - t1) % sp.H
+            out[:, t] = left[t0 - left_first] + torch.roll(right[t1 - right_first], -r)
+
+    def empty_out(self, sp, like):
+        return torch.zeros((sp.H, sp.W), dtype=torch.int64)
+
+
+def _root_worker(rank, world, port, out_path, quadrant, strategy):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2411_07351_b200.shard import root_split_quadrant
+
+    rng = np.random.default_rng(11)
+    img = torch.from_numpy(rng.integers(0, 1000, (37, 45)).astype(np.int64))
+    out, sp = root_split_quadrant(img, quadrant, strategy, side=rank, backend=_CpuRootBackend(strategy), peer=1 - rank)
+    np.save(f"{out_path}.{rank}.npy", out.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("quadrant,strategy", [("horiz_pos", 1), ("horiz_neg", 0), ("vert_pos", 1), ("vert_neg", 1)])
+def test_root_split_two_ranks_gloo(tmp_path, quadrant, strategy):
+    import oracle
+    from paper_2411_07351_b200.shard import root_split
+
+    out = tmp_path / "root"
+    mp.spawn(_root_worker, args=(2, _free_port(), str(out), quadrant, strategy), nprocs=2, join=True)
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 1000, (37, 45)).astype(np.int64)
+    ref, _ = oracle.fht2d_quadrants(img, strategy)
+    a, b = np.load(f"{out}.0.npy"), np.load(f"{out}.1.npy")
+    H, W = ref[quadrant].shape
+    sp = root_split(W, H, strategy)
+    np.testing.assert_array_equal(a[:, :sp.t_mid], ref[quadrant][:, :sp.t_mid])
+    np.testing.assert_array_equal(b[:, sp.t_mid:], ref[quadrant][:, sp.t_mid:])
