@@ -86,6 +86,7 @@ struct DevTables {
     const ShapeHdr* shapes = nullptr;
     const int* step_offs = nullptr;
     const fhtb::PassOpDev* k1_ops = nullptr;
+    const int4* k1_bops = nullptr;
     std::vector<fhtb::PassDev> passes;  // device pointers; S/L filled by create_plan
     int max_ops = 0, max_steps = 0;
 };
@@ -123,11 +124,16 @@ struct fht_plan_s {
     void* st_in = nullptr;
     void* st_out[4] = {nullptr, nullptr, nullptr, nullptr};
     void* st_ws = nullptr;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     ~fht_plan_s() {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
+        if (aux) cudaStreamDestroy(aux);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         for (auto& g : groups)
             if (g->dt.blob) cudaFree(g->dt.blob);
         if (st_in) cudaFree(st_in);
@@ -209,6 +215,20 @@ void upload(Group& g) {
     const size_t o_shapes = put(shapes.data(), shapes.size() * sizeof(ShapeHdr));
     const size_t o_steps = put(step_offs.data(), step_offs.size() * sizeof(int));
     const size_t o_k1 = put(k1_ops.data(), k1_ops.size() * sizeof(fhtb::PassOp));
+    // the same ops baked into shared byte offsets (slot stride sr) for the
+    // 4-byte vector executor: {dst, a, b aligned | (shift & 3) or -1, rows}
+    std::vector<int4> k1_bops;
+    {
+        size_t k = 0;
+        for (const auto& sh : sp.shapes)
+            for (size_t o = 0; o < sh.ops.size(); ++o, ++k) {
+                const fhtb::PassOp& po = k1_ops[k];
+                const int64_t d = int64_t(po.dst) * g.sr * 4, a = int64_t(po.a) * g.sr * 4;
+                const int64_t b = po.b < 0 ? -1 : ((int64_t(po.b) * g.sr + (po.bd & ~3)) * 4) | (po.bd & 3);
+                k1_bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(a), static_cast<int>(b), g.S + po.ext));
+            }
+    }
+    const size_t o_k1b = put(k1_bops.data(), k1_bops.size() * sizeof(int4));
     struct PassOff {
         size_t tiles, loads, steps, ops, stores, bops;
     };
@@ -250,6 +270,7 @@ void upload(Group& g) {
     g.dt.shapes = reinterpret_cast<const ShapeHdr*>(base + o_shapes);
     g.dt.step_offs = reinterpret_cast<const int*>(base + o_steps);
     g.dt.k1_ops = reinterpret_cast<const fhtb::PassOpDev*>(base + o_k1);
+    g.dt.k1_bops = reinterpret_cast<const int4*>(base + o_k1b);
     for (size_t i = 0; i < o_passes.size(); ++i) {
         const PassOff& o = o_passes[i];
         fhtb::PassDev d{};
@@ -305,6 +326,9 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
 
     auto p = std::make_unique<fht_plan_s>();
     cuda_check(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+    cuda_check(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "cudaEventCreate");
     p->w = w, p->h = h, p->strategy = strategy, p->in = in, p->acc = acc, p->out = out, p->mask = mask;
     p->batch = batch, p->layout = layout, p->device = device;
     const int bw = block_width_default();
@@ -439,9 +463,13 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.nby = g.nby;
             L.by_x0 = g.dt.by_x0;
             L.k1p_variant = env_int("FHT_K1P_VARIANT", 2, 0, 2);  // 2: levels 1-2 in registers
+            L.aux_stream = env_int("FHT_K1_OVERLAP", 1, 0, 1) ? p->aux : nullptr;
+            L.ev_fork = p->ev_fork;
+            L.ev_join = p->ev_join;
             L.shapes = g.dt.shapes;
             L.step_offs = g.dt.step_offs;
             L.k1_ops = g.dt.k1_ops;
+            L.k1_bops = g.dt.k1_bops;
             L.k1_max_ops = g.dt.max_ops;
             L.k1_max_steps = g.dt.max_steps;
             L.k1_max_width = g.sp.max_block_width;

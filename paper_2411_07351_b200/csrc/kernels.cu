@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const In* __restrict__ img, int img_w, int img_h, long long img_pitch, long long img_stride, int img0, QuadSet qs,
     int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
-    const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, int max_width, int sr, int max_ops,
+    const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, const int4* __restrict__ bops, int max_width,
+    int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
@@ -378,8 +379,12 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     // the buffer of that parity (ops carry parity-offset slot numbers).
     for (int k = 0; k < nsteps; ++k) {
         __syncthreads();
-        run_step<Acc, kWarps>(buf0, sr, ops + hdr.op_base, step_offs[hdr.step_base + k],
-                              step_offs[hdr.step_base + k + 1], S, warp, lane);
+        if constexpr (sizeof(Acc) == 4)
+            run_step_baked<Acc, kWarps>(smem_u32(buf0), bops + hdr.op_base, step_offs[hdr.step_base + k],
+                                        step_offs[hdr.step_base + k + 1], warp, lane);
+        else
+            run_step<Acc, kWarps>(buf0, sr, ops + hdr.op_base, step_offs[hdr.step_base + k],
+                                  step_offs[hdr.step_base + k + 1], S, warp, lane);
     }
     __syncthreads();
 
@@ -838,6 +843,24 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     auto k1 = k1_blocks<In, Acc, Out>;
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
+    // Pass 0: the width-32 Brady-Yong blocks (K1P) and the other blocks (K1)
+    // write disjoint columns; when both exist, K1 runs concurrently on the
+    // plan's auxiliary stream (joined by an event before the first K2 pass).
+    const bool both = (sizeof(Acc) == 4) && g.nby > 0 && g.nblocks > 0 && g.aux_stream && !hook;
+    cudaStream_t st1 = both ? g.aux_stream : st;
+    if (both) {
+        cudaEventRecord(g.ev_fork, st);
+        cudaStreamWaitEvent(st1, g.ev_fork, 0);
+    }
+    if (g.nblocks > 0) {
+        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
+        k1<<<g1, kThreads, smem, st1>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
+                                        g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes,
+                                        g.step_offs, g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws,
+                                        g.nbuf, g.root_is_block, g.out);
+        ++launches;
+        if (hook) hook(ctx, 1);
+    }
     if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
             auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 2>;
@@ -845,20 +868,14 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
             kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                              g.img_stride,
-                                              g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
+                                              g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
             ++launches;
             if (hook) hook(ctx, 4);
         }
     }
-    if (g.nblocks > 0) {
-        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
-        k1<<<g1, kThreads, smem, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                       g.img_stride, g.img0,
-                                       g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs, g.k1_ops,
-                                       g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out);
-        ++launches;
-        if (hook) hook(ctx, 1);
+    if (both) {
+        cudaEventRecord(g.ev_join, st1);
+        cudaStreamWaitEvent(st, g.ev_join, 0);
     }
     if (g.root_is_block) return launches;
     const long long slot_elems = (long long)g.nbuf * g.W * g.ld;

@@ -75,10 +75,13 @@ struct GroupLaunch {
     const int4* blocks;
     int nby;            // width-32 Brady-Yong blocks for the specialised K1P (4-byte accumulators)
     const int* by_x0;
+    cudaStream_t aux_stream;  // plan-owned stream for the concurrent generic-block K1 (may be null)
+    cudaEvent_t ev_fork, ev_join;
     int k1p_variant;    // 2 (default): levels 1-2 in registers; 0: all levels in shared memory
     const ShapeHdr* shapes;
     const int* step_offs;
     const PassOpDev* k1_ops;  // per-shape ops, slots pre-offset by buffer parity
+    const int4* k1_bops;      // the same, baked into shared byte offsets (4-byte accumulators)
     int k1_max_ops, k1_max_steps, k1_max_width, k1_sr;
     bool root_is_block;
     // fused upper passes (K2), in execution order; the last writes the root
