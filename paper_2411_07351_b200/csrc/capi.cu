@@ -104,6 +104,8 @@ struct Group {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+constexpr int kHostStreams = 3;
+
 int env_int(const char* name, int def, int lo, int hi) {
     if (const char* e = std::getenv(name)) return std::max(lo, std::min(hi, std::atoi(e)));
     return def;
@@ -126,12 +128,20 @@ struct fht_plan_s {
     void* st_ws = nullptr;
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t hst[kHostStreams] = {};  // execute_host pipeline
+    cudaEvent_t hev[kHostStreams] = {};
+    cudaEvent_t hev_start = nullptr;
 
     ~fht_plan_s() {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         if (aux) cudaStreamDestroy(aux);
+        for (int k = 0; k < kHostStreams; ++k) {
+            if (hst[k]) cudaStreamDestroy(hst[k]);
+            if (hev[k]) cudaEventDestroy(hev[k]);
+        }
+        if (hev_start) cudaEventDestroy(hev_start);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         for (auto& g : groups)
@@ -431,7 +441,9 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
 }
 
 void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_out[4], int64_t out_stride,
-             void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr, int64_t in_pitch = 0) {
+             void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr, int64_t in_pitch = 0,
+             int img_begin = 0, int img_end = -1) {
+    if (img_end < 0) img_end = p->batch;
     if (in_pitch == 0) in_pitch = p->w;
     if (in_pitch < p->w) throw std::invalid_argument("fht_execute: row pitch smaller than the image width");
     if (!d_in) throw std::invalid_argument("fht_execute: null input");
@@ -439,8 +451,8 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
         if ((p->mask & (1 << q)) && !d_out[q]) throw std::invalid_argument("fht_execute: null output for a selected quadrant");
     if (p->ws_bytes && !ws) throw std::invalid_argument("fht_execute: null workspace");
     DeviceGuard dg(p->device);
-    for (int img0 = 0; img0 < p->batch; img0 += p->chunk) {
-        const int nimg = std::min(p->chunk, p->batch - img0);
+    for (int img0 = img_begin; img0 < img_end; img0 += p->chunk) {
+        const int nimg = std::min(p->chunk, img_end - img0);
         for (auto& gp : p->groups) {
             Group& g = *gp;
             GroupLaunch L{};
@@ -491,23 +503,60 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
 
 size_t cells_of(const fht_plan_s* p) { return static_cast<size_t>(p->w) * p->h; }
 
+// Host buffers in and out.  For batches the images are cut into parts that
+// rotate over three plan-owned streams, so the H2D copy of one part, the
+// kernels of another and the D2H copies of a third overlap (PCIe is full
+// duplex; the transform itself is a few percent of the copy time).
 void execute_host(fht_plan_s* p, const void* h_in, void* const h_out[4], cudaStream_t st) {
     if (!h_in) throw std::invalid_argument("fht_execute_host: null input");
+    for (int q = 0; q < 4; ++q)
+        if ((p->mask & (1 << q)) && !h_out[q]) throw std::invalid_argument("fht_execute_host: null output for a selected quadrant");
     std::lock_guard<std::mutex> lk(p->host_mu);
     DeviceGuard dg(p->device);
     const size_t cells = cells_of(p);
-    const size_t in_bytes = cells * esize(p->in) * p->batch, out_bytes = cells * esize(p->out) * p->batch;
-    if (!p->st_in) cuda_check(cudaMalloc(&p->st_in, in_bytes), "cudaMalloc(staging in)");
+    const size_t in_img = cells * esize(p->in), out_img = cells * esize(p->out);
+    const int nparts = p->batch >= 2 ? std::min(p->batch, env_int("FHT_HOST_PARTS", 8, 1, 64)) : 1;
+    const int nst = nparts > 1 ? kHostStreams : 1;
+    const int per_part = (p->batch + nparts - 1) / nparts;
+    const size_t ws_per_img = p->chunk ? p->ws_bytes / static_cast<size_t>(p->chunk) : 0;
+    const size_t ws_part = ws_per_img * static_cast<size_t>(std::min(per_part, p->chunk));
+    if (!p->st_in) cuda_check(cudaMalloc(&p->st_in, in_img * p->batch), "cudaMalloc(staging in)");
     for (int q = 0; q < 4; ++q)
-        if ((p->mask & (1 << q)) && !p->st_out[q]) cuda_check(cudaMalloc(&p->st_out[q], out_bytes), "cudaMalloc(staging out)");
-    if (p->ws_bytes && !p->st_ws) cuda_check(cudaMalloc(&p->st_ws, p->ws_bytes), "cudaMalloc(workspace)");
-    cuda_check(cudaMemcpyAsync(p->st_in, h_in, in_bytes, cudaMemcpyHostToDevice, st), "H2D");
-    execute(p, p->st_in, static_cast<int64_t>(cells), p->st_out, static_cast<int64_t>(cells), p->st_ws, st);
-    for (int q = 0; q < 4; ++q)
-        if (p->mask & (1 << q)) {
-            if (!h_out[q]) throw std::invalid_argument("fht_execute_host: null output for a selected quadrant");
-            cuda_check(cudaMemcpyAsync(h_out[q], p->st_out[q], out_bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        if ((p->mask & (1 << q)) && !p->st_out[q])
+            cuda_check(cudaMalloc(&p->st_out[q], out_img * p->batch), "cudaMalloc(staging out)");
+    if (ws_part && !p->st_ws) cuda_check(cudaMalloc(&p->st_ws, ws_part * nst), "cudaMalloc(workspace)");
+    if (nst > 1 && !p->hst[0]) {
+        for (int k = 0; k < kHostStreams; ++k) {
+            cuda_check(cudaStreamCreateWithFlags(&p->hst[k], cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(cudaEventCreateWithFlags(&p->hev[k], cudaEventDisableTiming), "cudaEventCreate");
         }
+        cuda_check(cudaEventCreateWithFlags(&p->hev_start, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    if (nst > 1) {  // order after the caller's stream
+        cuda_check(cudaEventRecord(p->hev_start, st), "cudaEventRecord");
+        for (int k = 0; k < nst; ++k) cuda_check(cudaStreamWaitEvent(p->hst[k], p->hev_start, 0), "cudaStreamWaitEvent");
+    }
+    for (int part = 0; part < nparts; ++part) {
+        const int b = part * per_part, e = std::min(p->batch, b + per_part);
+        if (b >= e) break;
+        cudaStream_t s = nst > 1 ? p->hst[part % nst] : st;
+        char* ws = static_cast<char*>(p->st_ws) + (nst > 1 ? (part % nst) * ws_part : 0);
+        cuda_check(cudaMemcpyAsync(static_cast<char*>(p->st_in) + b * in_img, static_cast<const char*>(h_in) + b * in_img,
+                                   (e - b) * in_img, cudaMemcpyHostToDevice, s), "H2D");
+        execute(p, p->st_in, static_cast<int64_t>(cells), p->st_out, static_cast<int64_t>(cells), ws, s, nullptr, nullptr,
+                0, b, e);
+        for (int q = 0; q < 4; ++q)
+            if (p->mask & (1 << q))
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(h_out[q]) + b * out_img,
+                                           static_cast<char*>(p->st_out[q]) + b * out_img, (e - b) * out_img,
+                                           cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    if (nst > 1) {
+        for (int k = 0; k < nst; ++k) {
+            cuda_check(cudaEventRecord(p->hev[k], p->hst[k]), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(st, p->hev[k], 0), "cudaStreamWaitEvent");
+        }
+    }
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
 }
 
