@@ -224,8 +224,8 @@ uint64_t oracle_count_additions_tree(int w, int h, int strategy) {
 /*
  * CPU-baseline helper (port flavour of oracle/ref_shim.cpp's
  * ref_batch_quadrants_u8): n_img uint8 images, the quadrants in
- * quadrant_mask, widened to int64, `threads` pthreads over images.
- * If out is non-null image i's four Hough images go to out + i*4*w*h.
+ * quadrant_mask, widened to int64, `threads` pthreads over (image, quadrant)
+ * items.  If out is non-null image i's quadrant q goes to out + (i*4+q)*w*h.
  */
 #include <pthread.h>
 
@@ -241,24 +241,38 @@ typedef struct {
 static void* batch_worker(void* arg) {
     batch_job* j = (batch_job*)arg;
     size_t cells = (size_t)j->w * (size_t)j->h;
+    int quads[4], nq = 0;
+    for (int q = 0; q < 4; ++q)
+        if (j->mask & (1 << q)) quads[nq++] = q;
     int64_t* in = (int64_t*)malloc(sizeof(int64_t) * cells);
-    int64_t* q[4];
-    for (int k = 0; k < 4; ++k) q[k] = (int64_t*)malloc(sizeof(int64_t) * cells);
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * cells);
+    int64_t* res = (int64_t*)malloc(sizeof(int64_t) * cells);
     for (;;) {
         pthread_mutex_lock(&j->mu);
-        int i = j->next++;
+        int k = j->next++;
         pthread_mutex_unlock(&j->mu);
-        if (i >= j->n_img) break;
+        if (k >= j->n_img * nq) break;
+        int i = k / nq, q = quads[k % nq];
         const uint8_t* src = j->img + (size_t)i * cells;
-        for (size_t k = 0; k < cells; ++k) in[k] = src[k];
-        int rc = oracle_fht2d_quadrants_i64(in, j->w, j->h, j->strategy, q[0], q[1], q[2], q[3], 0);
+        int W = j->w, H = j->h;
+        /* the quadrant's input as fht2d_quadrants builds it (quadrants.cpp:25-37) */
+        for (int y = 0; y < j->h; ++y)
+            for (int x = 0; x < j->w; ++x) {
+                int64_t v = src[(size_t)y * j->w + x];
+                if (q == 0) in[(size_t)y * j->w + x] = v;
+                else if (q == 1) in[(size_t)y * j->w + (j->w - 1 - x)] = v;
+                else if (q == 2) in[(size_t)x * j->h + y] = v;
+                else in[(size_t)x * j->h + (j->h - 1 - y)] = v;
+            }
+        if (q >= 2) { W = j->h; H = j->w; }
+        (void)tmp;
+        int rc = oracle_fht2d_i64(in, W, H, j->strategy, res, 0);
         if (rc) { j->rc = rc; break; }
-        if (j->out)
-            for (int k = 0; k < 4; ++k)
-                if (j->mask & (1 << k)) memcpy(j->out + ((size_t)i * 4 + k) * cells, q[k], sizeof(int64_t) * cells);
+        if (j->out) memcpy(j->out + ((size_t)i * 4 + q) * cells, res, sizeof(int64_t) * cells);
     }
     free(in);
-    for (int k = 0; k < 4; ++k) free(q[k]);
+    free(tmp);
+    free(res);
     return 0;
 }
 

@@ -15,9 +15,10 @@
 // overflow_error, 4 anything else; the message goes to `err`.
 //
 // ref_batch_quadrants_u8 is the CPU baseline used by bench.py: it runs the
-// reference fht2d_quadrants on a batch of uint8 images with a pool of host
-// threads (images across threads; the reference is safe to call
+// reference's per-quadrant transforms on a batch of uint8 images with a pool
+// of host threads over (image, quadrant) items (the reference is safe to call
 // concurrently).
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -110,60 +111,49 @@ uint64_t ref_count_additions_tree(int w, int h, int strategy) {
     return fht::count_additions_tree(w, h, strat(strategy));
 }
 
-// CPU baseline: n_img uint8 images (image i at img + i*w*h), all four
-// quadrants each, `threads` host threads pulling images from a shared
-// counter.  If `out` is non-null the four int64 Hough images of image i are
-// written at out + i*4*w*h (horiz_pos, horiz_neg, vert_pos, vert_neg).
-// quadrant_mask selects a subset: bit q runs quadrant q through
-// fht2d_counted on the same flipped/transposed input the reference builds.
+// CPU baseline: n_img uint8 images (image i at img + i*w*h), the quadrants
+// in quadrant_mask, widened to int64 and transformed by the reference:
+// work items (image, quadrant) are pulled from a shared counter by `threads`
+// host threads (concurrent calls are safe), so a single
+// image's four quadrants also run in parallel.  Item (i, q) runs
+// fht2d_counted on the same flipped / transposed input fht2d_quadrants
+// builds (quadrants.cpp:25-37).  If `out` is non-null image i's quadrant q
+// goes to out + (i*4 + q)*w*h.
 int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int strategy,
                            int quadrant_mask, int threads, int64_t* out, char* err, int errlen) {
     return guarded(err, errlen, [&] {
         const std::size_t cells = static_cast<std::size_t>(w) * h;
+        std::vector<int> quads;
+        for (int q = 0; q < 4; ++q)
+            if (quadrant_mask & (1 << q)) quads.push_back(q);
+        const int n_items = n_img * static_cast<int>(quads.size());
         std::atomic<int> next{0};
         std::atomic<int> failed{0};
         std::string first_error;
         auto worker = [&] {
             for (;;) {
-                const int i = next.fetch_add(1);
-                if (i >= n_img || failed.load()) return;
+                const int k = next.fetch_add(1);
+                if (k >= n_items || failed.load()) return;
+                const int i = k / static_cast<int>(quads.size()), q = quads[static_cast<std::size_t>(k) % quads.size()];
                 try {
                     std::vector<int64_t> v(cells);
                     const uint8_t* src = img + static_cast<std::size_t>(i) * cells;
-                    for (std::size_t k = 0; k < cells; ++k) v[k] = src[k];
+                    for (std::size_t c = 0; c < cells; ++c) v[c] = src[c];
                     fht::Image im(w, h, std::move(v));
-                    int64_t* dst = out ? out + static_cast<std::size_t>(i) * 4 * cells : nullptr;
-                    if (quadrant_mask == 0xF) {
-                        fht::QuadrantSet q = fht::fht2d_quadrants(im, strat(strategy));
-                        if (dst) {
-                            copy_out(q.horiz_pos, dst);
-                            copy_out(q.horiz_neg, dst + cells);
-                            copy_out(q.vert_pos, dst + 2 * cells);
-                            copy_out(q.vert_neg, dst + 3 * cells);
-                        }
-                    } else {
-                        const fht::Image tr = fht::transpose(im);
-                        const fht::Image* inputs[4] = {nullptr, nullptr, nullptr, nullptr};
-                        fht::Image flipped, flipped_tr;
-                        if (quadrant_mask & 2) flipped = fht::flip_horizontal(im);
-                        if (quadrant_mask & 8) flipped_tr = fht::flip_horizontal(tr);
-                        inputs[0] = &im;
-                        inputs[1] = &flipped;
-                        inputs[2] = &tr;
-                        inputs[3] = &flipped_tr;
-                        for (int q = 0; q < 4; ++q) {
-                            if (!(quadrant_mask & (1 << q))) continue;
-                            fht::CountedTransform r = fht::fht2d_counted(*inputs[q], strat(strategy));
-                            if (dst) copy_out(r.hough, dst + q * cells);
-                        }
-                    }
+                    fht::Image input;
+                    if (q == 0) input = std::move(im);
+                    else if (q == 1) input = fht::flip_horizontal(im);
+                    else if (q == 2) input = fht::transpose(im);
+                    else input = fht::flip_horizontal(fht::transpose(im));
+                    fht::CountedTransform r = fht::fht2d_counted(input, strat(strategy));
+                    if (out) copy_out(r.hough, out + (static_cast<std::size_t>(i) * 4 + q) * cells);
                 } catch (const std::exception& e) {
                     if (!failed.exchange(1)) first_error = e.what();
                     return;
                 }
             }
         };
-        const int nt = threads < 1 ? 1 : threads;
+        const int nt = std::max(1, std::min(threads, n_items));
         std::vector<std::thread> pool;
         for (int k = 1; k < nt; ++k) pool.emplace_back(worker);
         worker();
