@@ -88,7 +88,7 @@ int oracle_check_overflow_budget(const int64_t* data, int w, int h) {
             memcpy(out, in, sizeof(T) * (size_t)h);                                             \
             return;                                                                             \
         }                                                                                       \
-        int w0, w1;                                                                             \
+        int w0 = 0, w1 = 0;                                                                     \
         oracle_split(w, strategy, &w0, &w1);                                                    \
         size_t left = (size_t)w0 * (size_t)h;                                                   \
         cols_##SUF(in, tmp, out, w0, h, strategy, additions);                                   \
@@ -178,7 +178,7 @@ static void build_values(int* out, int n, int t, int lift, int strategy) {
         out[0] = lift;
         return;
     }
-    int n0, n1;
+    int n0 = 0, n1 = 0;
     oracle_split(n, strategy, &n0, &n1);
     int t0 = (int)oracle_rhu((int64_t)t * (n0 - 1), n - 1);
     int t1 = (int)oracle_rhu((int64_t)t * (n1 - 1), n - 1);
