@@ -15,6 +15,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -835,13 +838,25 @@ __global__ void k_absmax(const T* __restrict__ in, long long n, unsigned long lo
 }
 
 // ------------------------------------------------------------ launchers
+// Opt a kernel into the full 227 KB of dynamic shared memory once per
+// (device, kernel) instead of on every launch (host overhead on small images).
+void allow_smem(const void* fn) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({dev, fn}).second)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
 template <class In, class Acc, class Out>
 int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* ctx) {
     int launches = 0;
     const int nslots = g.nimg * g.qs.n;
     const size_t smem = k1_smem_bytes(g.acc_dtype, g.k1_max_width, g.k1_sr, g.k1_max_ops, g.k1_max_steps);
     auto k1 = k1_blocks<In, Acc, Out>;
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    allow_smem(reinterpret_cast<const void*>(k1));
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
     // Pass 0: the width-32 Brady-Yong blocks (K1P) and the other blocks (K1)
     // write disjoint columns; when both exist, K1 runs concurrently on the
@@ -865,7 +880,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         if (g.nby > 0) {
             auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 2>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
-            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_by);
+            allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
             kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
                                               g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
@@ -886,7 +901,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
         auto k2 = k2_pass<Acc, Out>;
-        cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+        allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
         k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
         ++launches;
