@@ -172,6 +172,12 @@ int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, 
  * <-> fht::fht2d_pattern (pattern.hpp:20, pattern.cpp:24-30). */
 int fht_fht2d_pattern(int n, int t, int strategy, int* values);
 
+/* The paper's accuracy sweep on the device (analysis.cpp:63-91): for each
+ * width n in [n_lo, n_hi] (<= 46340), worst[n - n_lo] = max over slopes t and
+ * columns x of |x t - pat(n,t)(x) (n-1)|, i.e. E(n) = worst / (n-1) exactly
+ * (max_orthotropic_error, analysis.hpp:39).  Synchronous. */
+int fht_max_deviation_numerators(int n_lo, int n_hi, int strategy, int64_t* worst);
+
 /* Host helpers, identical to the reference's integer rules. */
 int fht_split_width(int w, int strategy, int* w0, int* w1);                 /* split.hpp:46-48 */
 int fht_round_half_up_ratio(int64_t num, int64_t den, int64_t* result);     /* split.hpp:53-57 */

@@ -27,6 +27,7 @@
 #include <thread>
 #include <vector>
 
+#include "fht/analysis.hpp"
 #include "fht/oracle.hpp"
 #include "fht/pattern.hpp"
 #include "fht/quadrants.hpp"
@@ -159,6 +160,31 @@ int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int stra
         worker();
         for (auto& t : pool) t.join();
         if (failed.load()) throw std::runtime_error(first_error);
+    });
+}
+
+// analysis.hpp:37-62 (paper-figure reproduction): exact rationals as (num, den).
+int ref_max_orthotropic_error(int n, int strategy, int64_t* num, int64_t* den, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const fht::Rational r = fht::max_orthotropic_error(n, strat(strategy));
+        *num = r.num();
+        *den = r.den();
+    });
+}
+
+int ref_separation_fraction(int n_max, int threads, int64_t* num, int64_t* den, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const fht::Rational r = fht::separation_fraction(n_max, static_cast<unsigned>(threads));
+        *num = r.num();
+        *den = r.den();
+    });
+}
+
+int ref_tweaked_error_bound(int n, int64_t* num, int64_t* den, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const fht::Rational r = fht::tweaked_error_bound(n);
+        *num = r.num();
+        *den = r.den();
     });
 }
 

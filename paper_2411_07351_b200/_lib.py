@@ -45,6 +45,7 @@ SIGNATURES = {
     "fht_slow_hough_device": (_i, [_vp, _i, _i, _i, _i, _i, _pi64, _vp]),
     "fht_slow_hough_i64": (_i, [_pi64, _i, _i, _i, _pi64]),
     "fht_fht2d_pattern": (_i, [_i, _i, _i, _pi]),
+    "fht_max_deviation_numerators": (_i, [_i, _i, _i, _pi64]),
     "fht_split_width": (_i, [_i, _i, _pi, _pi]),
     "fht_round_half_up_ratio": (_i, [_i64, _i64, _pi64]),
     "fht_count_additions_tree": (_i, [_i, _i, _i, _pu64]),

@@ -882,6 +882,28 @@ int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, 
     });
 }
 
+int fht_max_deviation_numerators(int n_lo, int n_hi, int strategy, int64_t* worst) {
+    return guarded([&] {
+        if (n_lo < 1 || n_hi < n_lo || n_hi > 46340) throw std::invalid_argument("max_deviation: need 1 <= n_lo <= n_hi <= 46340");
+        if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED) throw std::invalid_argument("unknown strategy");
+        if (!worst) throw std::invalid_argument("max_deviation: null output");
+        const size_t cnt = static_cast<size_t>(n_hi - n_lo + 1);
+        cudaStream_t st = cudaStreamPerThread;
+        unsigned long long* d = nullptr;
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d), cnt * 8, st), "cudaMallocAsync");
+        cuda_check(cudaMemsetAsync(d, 0, cnt * 8, st), "cudaMemsetAsync");
+        // slices of widths keep each launch's grid.y and run time bounded
+        for (int a = n_lo; a <= n_hi; a += 8192) {
+            const int b = std::min(n_hi, a + 8191);
+            fhtb::launch_max_deviation(a, b, strategy, d + (a - n_lo), st);
+        }
+        cuda_check(cudaGetLastError(), "max_deviation launch");
+        cuda_check(cudaMemcpyAsync(worst, d, cnt * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaFreeAsync(d, st), "cudaFreeAsync");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    });
+}
+
 int fht_split_width(int w, int strategy, int* w0, int* w1) {
     return guarded([&] {
         if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED) throw std::invalid_argument("unknown strategy");

@@ -65,3 +65,60 @@ void launch_slow_hough(const void* img, int in_dtype, int img_w, int img_h, int 
 }
 
 }  // namespace fhtb
+
+// ------------------------------------------------------------- analysis
+// The paper's accuracy sweep (analysis.cpp:63-91, 231-243) on the device:
+// for every width n and slope t, max over x of |x t - pat(n,t)(x) (n-1)|, the
+// numerator of the max orthotropic error E(n) = worst / (n-1).  pat(n,t)(x)
+// is found by descending Algorithm 2's split tree from the root (pattern.cpp:
+// 10-20): O(log n) per point, no tables; unsigned 32-bit products are exact
+// for n <= 46340.
+namespace fhtb {
+namespace {
+
+__device__ __forceinline__ unsigned pattern_value(unsigned n, unsigned t, unsigned x, int strategy) {
+    unsigned w = n, x0 = 0, tn = t, lift = 0;
+    while (w > 1) {
+        const unsigned w0 = strategy == 0 ? (w >> 1) : (1u << (31 - __clz(w - 1)));  // split.hpp:33-44
+        const unsigned w1 = w - w0, den2 = 2 * (w - 1);
+        if (x < x0 + w0) {
+            tn = (2 * tn * (w0 - 1) + (w - 1)) / den2;  // round_half_up_ratio, split.hpp:53-57
+            w = w0;
+        } else {
+            const unsigned t1 = (2 * tn * (w1 - 1) + (w - 1)) / den2;
+            lift += tn - t1;
+            tn = t1;
+            x0 += w0;
+            w = w1;
+        }
+    }
+    return lift;
+}
+
+// grid: x = chunk of 8 slopes, y = n - n_lo; warp per slope, lanes over x.
+__global__ void k_max_deviation(int n_lo, int strategy, unsigned long long* __restrict__ worst) {
+    const unsigned n = n_lo + blockIdx.y;
+    const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t >= n) return;  // warp-uniform
+    const unsigned lane = threadIdx.x & 31;
+    unsigned long long m = 0;
+    for (unsigned x = lane; x < n; x += 32) {
+        const long long d = (long long)x * t - (long long)pattern_value(n, t, x, strategy) * (long long)(n - 1);
+        const unsigned long long a = d < 0 ? -d : d;
+        m = a > m ? a : m;
+    }
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, m, off);
+        m = o > m ? o : m;
+    }
+    if (lane == 0) atomicMax(worst + blockIdx.y, m);
+}
+
+}  // namespace
+
+void launch_max_deviation(int n_lo, int n_hi, int strategy, unsigned long long* d_worst, cudaStream_t st) {
+    dim3 g((n_hi + 7) / 8, n_hi - n_lo + 1);
+    k_max_deviation<<<g, 256, 0, st>>>(n_lo, strategy, d_worst);
+}
+
+}  // namespace fhtb

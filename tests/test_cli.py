@@ -117,3 +117,42 @@ def test_transform_c1_size(tmp_path):
     r = run("transform", "--input", src, "--strategy", "tweaked", "--output", tmp_path / "c1.fht1")
     assert r.returncode == 0, r.stderr
     np.testing.assert_array_equal(read_fht1(tmp_path / "c1.fht1"), oracle.fht2d_counted_i64(img, 1)[0])
+
+
+def test_analyze_complexity_csv(tmp_path):
+    from paper_2411_07351_b200 import analysis
+
+    out = tmp_path / "c.csv"
+    r = run("analyze", "complexity", "--n-max", 70, "--output", out)
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().splitlines()
+    assert lines[0] == "n,f_simple,f_tweaked,norm_simple,norm_tweaked"
+    for line, rec in zip(lines[1:], analysis.complexity_series(70)):
+        n, fs, ft, ns, nt = line.split(",")
+        assert (int(n), int(fs), int(ft)) == (rec.n, rec.f_simple, rec.f_tweaked)
+        if rec.n > 1:
+            assert ns == "%.12g" % rec.norm_simple and nt == "%.12g" % rec.norm_tweaked
+    assert lines[17].split(",")[2] == "1377"  # f_T(17)
+
+
+@pytest.mark.gpu
+def test_analyze_error_fast_csv(tmp_path):
+    from fractions import Fraction
+
+    gold = np.load(ROOT / "tests" / "golden" / "analysis_vectors.npz")
+    out = tmp_path / "e.csv"
+    r = run("analyze", "error", "--n-max", 1500, "--fast", "--output", out)
+    assert r.returncode == 0, r.stderr
+    rows = [l.split(",") for l in out.read_text().splitlines()[1:]]
+    assert [int(x[0]) for x in rows] == list(range(1, 1025)) + [1451]
+    ref = {int(g[0]): g for g in gold["errors"]}
+    exceeding = 0
+    for x in rows:
+        n = int(x[0])
+        g = ref[n]
+        es, et = Fraction(int(g[1]), int(g[2])), Fraction(int(g[3]), int(g[4]))
+        assert x[1] == "%.12g" % float(es) and x[2] == "%.12g" % float(et), n
+        q = n.bit_length() - 1
+        bound = Fraction(q * (1 << q) + 6 * (1 << q) - 6, 6 * (1 << q))
+        exceeding += es > bound
+    assert r.stdout.strip() == "%.12g" % (exceeding / len(rows))

@@ -1,11 +1,12 @@
 // fht2d_b200 -- the reference CLI's transform path on the GPU.
 //
-// Mirrors `fht2d transform` / `fht2d pattern` of the reference CLI
-// (tools/fht2d_main.cpp:52-79, 112-175) with the same options, file formats
+// Mirrors `fht2d transform` / `pattern` / `analyze` of the reference CLI
+// (tools/fht2d_main.cpp:52-108, 112-175) with the same options, file formats
 // and exit behaviour:
 //   fht2d_b200 transform --input a.pgm --strategy simple|tweaked --output j.fht1|j.csv
 //                        [--count] [--quadrants]
 //   fht2d_b200 pattern --n N --t T --strategy simple|tweaked
+//   fht2d_b200 analyze complexity|error --n-max N [--fast] --output OUT.csv
 // Input: PGM P2/P5, maxval <= 65535, w*h <= 2^30 (pgm.cpp:42-87).  Output: the
 // FHT1 raster (magic "FHT1", u32 LE width/height, dtype byte 0, int64 LE
 // payload, x fastest; raster.hpp:10-19) or, for a .csv path, one line per shift
@@ -16,6 +17,8 @@
 // on the host); the transform accumulates in int32 when width * maxval < 2^31
 // (always for 8-bit input below 8.4M columns) and int64 otherwise, and the
 // root pass widens to int64 on the device.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -213,10 +216,91 @@ int run_pattern(int n, int t, int strategy) {
     return 0;
 }
 
+// ---------------------------------------------------------------- analyze
+// fht2d_main.cpp:81-108 with the csv.cpp layouts; the Theta(n^3) error sweep
+// runs on the GPU (fht_max_deviation_numerators).
+std::string sig(double v) {  // csv.cpp:10-16: 12 significant digits, general format
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.12g", v);
+    return buf;
+}
+
+int floor_log2i(int64_t n) {
+    int q = 0;
+    while ((int64_t(1) << (q + 1)) <= n) ++q;
+    return q;
+}
+
+int run_analyze(const std::string& mode, int n_max, bool fast, const std::string& output) {
+    if (n_max < 1) fail("--n-max must be positive");
+    std::ofstream out(output, std::ios::trunc);
+    if (!out) fail("cannot open '" + output + "' for writing");
+    if (mode == "complexity") {
+        out << "n,f_simple,f_tweaked,norm_simple,norm_tweaked\n";
+        for (int n = 1; n <= n_max; ++n) {
+            uint64_t fs = 0, ft = 0;
+            check(fht_count_additions_tree(n, n, FHT_SPLIT_SIMPLE, &fs));
+            check(fht_count_additions_tree(n, n, FHT_SPLIT_TWEAKED, &ft));
+            out << n << ',' << fs << ',' << ft << ',';
+            if (n > 1) {
+                const double d = static_cast<double>(n) * static_cast<double>(n) * std::log2(static_cast<double>(n));
+                out << sig(static_cast<double>(fs) / d) << ',' << sig(static_cast<double>(ft) / d);
+            } else {
+                out << ',';
+            }
+            out << '\n';
+        }
+    } else if (mode == "error") {
+        std::vector<int> sizes;
+        for (int n = 1; n <= (fast ? std::min(n_max, 1024) : n_max); ++n) sizes.push_back(n);
+        if (fast)
+            for (int s : {1451, 2048, 4095, 4096})
+                if (s <= n_max) sizes.push_back(s);
+        const int lo = 1, hi = fast ? std::min(n_max, 1024) : n_max;
+        std::vector<int64_t> ws(static_cast<size_t>(hi)), wt(static_cast<size_t>(hi));
+        check(fht_max_deviation_numerators(lo, hi, FHT_SPLIT_SIMPLE, ws.data()));
+        check(fht_max_deviation_numerators(lo, hi, FHT_SPLIT_TWEAKED, wt.data()));
+        out << "n,e_simple,e_tweaked,bound,norm_simple,norm_tweaked\n";
+        int64_t exceeding = 0;
+        for (int n : sizes) {
+            int64_t a = 0, b = 0;
+            if (n <= hi) {
+                a = ws[static_cast<size_t>(n - 1)];
+                b = wt[static_cast<size_t>(n - 1)];
+            } else {
+                check(fht_max_deviation_numerators(n, n, FHT_SPLIT_SIMPLE, &a));
+                check(fht_max_deviation_numerators(n, n, FHT_SPLIT_TWEAKED, &b));
+            }
+            const int64_t den = n == 1 ? 1 : n - 1;
+            const int q = floor_log2i(n);
+            const int64_t p = int64_t(1) << q, bnum = q * p + 6 * p - 6, bden = 6 * p;  // analysis.cpp:23-28
+            const double es = static_cast<double>(a) / static_cast<double>(den);
+            const double et = static_cast<double>(b) / static_cast<double>(den);
+            out << n << ',' << sig(es) << ',' << sig(et) << ',' << sig(static_cast<double>(bnum) / static_cast<double>(bden))
+                << ',';
+            if (n > 1) {
+                const double sc = 6.0 / std::log2(static_cast<double>(n));
+                out << sig(es * sc) << ',' << sig(et * sc);
+            } else {
+                out << ',';
+            }
+            out << '\n';
+            // e_simple > bound, exactly: a / den > bnum / bden
+            if (static_cast<__int128>(a) * bden > static_cast<__int128>(bnum) * den) ++exceeding;
+        }
+        std::cout << sig(static_cast<double>(exceeding) / static_cast<double>(sizes.size())) << "\n";
+    } else {
+        fail("unknown analyze mode '" + mode + "' (expected complexity|error)");
+    }
+    if (!out) fail("write failed for '" + output + "'");
+    return 0;
+}
+
 void usage() {
     std::cerr << "usage: fht2d_b200 transform --input IMG.pgm --strategy simple|tweaked --output OUT[.csv]"
                  " [--count] [--quadrants]\n"
-                 "       fht2d_b200 pattern --n N --t T --strategy simple|tweaked\n";
+                 "       fht2d_b200 pattern --n N --t T --strategy simple|tweaked\n"
+                 "       fht2d_b200 analyze complexity|error --n-max N [--fast] --output OUT.csv\n";
 }
 
 }  // namespace
@@ -228,8 +312,9 @@ int main(int argc, char** argv) {
     }
     const std::string cmd = argv[1];
     std::string input, output, strategy;
-    bool count = false, quadrants = false, have_n = false, have_t = false;
-    int n = 0, t = 0;
+    bool count = false, quadrants = false, have_n = false, have_t = false, fast = false;
+    int n = 0, t = 0, n_max = 0;
+    std::string mode;
     try {
         for (int i = 2; i < argc; ++i) {
             const std::string a = argv[i];
@@ -244,6 +329,9 @@ int main(int argc, char** argv) {
             else if (a == "--quadrants") quadrants = true;
             else if (a == "--n") n = std::stoi(value()), have_n = true;
             else if (a == "--t") t = std::stoi(value()), have_t = true;
+            else if (a == "--n-max") n_max = std::stoi(value());
+            else if (a == "--fast") fast = true;
+            else if (cmd == "analyze" && mode.empty() && a.rfind("--", 0) != 0) mode = a;
             else if (a == "-h" || a == "--help") {
                 usage();
                 return 0;
@@ -260,7 +348,11 @@ int main(int argc, char** argv) {
             if (!have_n || !have_t || strategy.empty()) fail("pattern requires --n, --t and --strategy");
             return run_pattern(n, t, strategy_of(strategy));
         }
-        fail("unknown subcommand '" + cmd + "' (expected transform|pattern)");
+        if (cmd == "analyze") {
+            if (mode.empty() || output.empty()) fail("analyze requires a mode, --n-max and --output");
+            return run_analyze(mode, n_max, fast, output);
+        }
+        fail("unknown subcommand '" + cmd + "' (expected transform|pattern|analyze)");
     } catch (const std::exception& e) {
         std::cerr << "fht2d: " << e.what() << "\n";
         return 1;
