@@ -1,16 +1,20 @@
 // kernels.cu -- sm_100a kernels for the FHT2D merge DP (transform.cpp:35-58).
 //
-// K1 k1_blocks : load an input tile in the quadrant's orientation straight
-//                from the row-major image (no flip / transpose copies,
-//                quadrants.cpp:7-21) and run every level of one block
-//                (maximal subtree of width <= block_width) in shared memory.
-// K2 k2_level  : one upper merge level, OUT[t] = IN[a] + rot(IN[b], r), as a
-//                coalesced, vectorised HBM/L2 ping-pong pass.
-// K3 k3_root   : the root level fused with the store into the reference
-//                layout hough[s*W + t] (transform.cpp:80-83) through an smem
-//                transpose, optionally widening to int64.
-// The path is a gather-add: no contraction, so no tensor cores; every kernel
-// is bound by HBM (or L2) bandwidth.  See DESIGN.md for the roofline model.
+// Pass 0 (blocks: maximal subtrees of width <= 32), loading the input tile in
+// the quadrant's orientation straight from the row-major image (no flip /
+// transpose copies, quadrants.cpp:7-21):
+//   k1_by32      K1P: width-32 Brady-Yong blocks, op indices computed
+//                arithmetically, levels 1-2 in registers, 3-5 in shared memory.
+//   k1_blocks    K1: any other block shape, table-driven ops.
+// Passes 1.. (the tree above the blocks in bands of <= 4 levels):
+//   k2_pass      K2: one tile program per CTA (cp.async windows of the
+//                frontier columns, merge ops level by level in shared memory);
+//                the last band stores the root in the reference layout
+//                hough[s*W + t] (transform.cpp:80-83), optionally widened.
+// Plus k_merge_root (the multi-GPU root split) and k_absmax (overflow budget).
+// The path is a gather-add: no contraction, so no tensor cores.  Each level
+// costs a shared-memory round trip per cell, so the kernels are bound by the
+// shared-memory/LSU pipe at this design point; see DESIGN.md §4.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -164,35 +168,6 @@ __device__ __forceinline__ void rows_op(uint32_t d, uint32_t a, uint32_t bb, int
     }
 }
 
-template <class Acc>
-__device__ __forceinline__ void rows_op_any(uint32_t d, uint32_t a, uint32_t b, int bd, int n, int lane) {
-    const uint32_t bb = b + static_cast<uint32_t>(bd & ~3) * 4u;
-    switch (bd & 3) {
-        case 0: rows_op<0, Acc>(d, a, bb, n, lane); break;
-        case 1: rows_op<1, Acc>(d, a, bb, n, lane); break;
-        case 2: rows_op<2, Acc>(d, a, bb, n, lane); break;
-        default: rows_op<3, Acc>(d, a, bb, n, lane); break;
-    }
-}
-
-// 4 consecutive rows per lane, lanes contiguous (conflict-free 16-byte
-// accesses): d[i..i+4) = a[i..i+4) + bb[i+M .. i+M+4), d, a, bb 16-byte
-// aligned.  M = (shift & 3) is warp-uniform, so the selection is static.
-template <int M, class Acc>
-__device__ __forceinline__ void merge_rows4(Acc* __restrict__ d, const Acc* __restrict__ a,
-                                            const Acc* __restrict__ bb, int n, int lane) {
-    for (int i = lane * 4; i < n; i += 128) {
-        const int4 a4 = lds4(a + i);
-        const int4 b0 = lds4(bb + i);
-        const int4 b1 = M ? lds4(bb + i + 4) : b0;
-        const int bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        sts4(d + i, make_int4(to_bits<Acc>(from_bits<Acc>(a4.x) + from_bits<Acc>(bv[M + 0])),
-                              to_bits<Acc>(from_bits<Acc>(a4.y) + from_bits<Acc>(bv[M + 1])),
-                              to_bits<Acc>(from_bits<Acc>(a4.z) + from_bits<Acc>(bv[M + 2])),
-                              to_bits<Acc>(from_bits<Acc>(a4.w) + from_bits<Acc>(bv[M + 3]))));
-    }
-}
-
 // K2 window load, 4-byte types: d[i] = col[(start + i) mod H], i < n, with
 // d 16-byte aligned.  The run up to the wrap point is copied with 16-byte
 // loads/stores when `start` is 4-aligned (columns are: ld % 4 == 0); the
@@ -222,29 +197,6 @@ __device__ __forceinline__ void warp_load_window_v(Acc* __restrict__ d, const Ac
         }
     }
     if (done < n) warp_load_window(d + done, col, wrap_any(start + done, H), n - done, H, lane);
-}
-
-// Shared-memory merge of one column window, d[i] = a[i] + b[bd + i] for
-// i < n (b null: copy), one warp.  4-byte types use the vector path (d, a
-// and the b slot base 16-byte aligned; rows up to bd + n + 8 are touched --
-// the slots carry that slack); int64 uses the scalar path.
-template <class Acc>
-__device__ __forceinline__ void warp_merge_any(Acc* d, const Acc* a, const Acc* b, int bd, int n, int lane) {
-    if constexpr (sizeof(Acc) == 4) {
-        if (b) {
-            const Acc* bb = b + (bd & ~3);
-            switch (bd & 3) {
-                case 0: merge_rows4<0>(d, a, bb, n, lane); break;
-                case 1: merge_rows4<1>(d, a, bb, n, lane); break;
-                case 2: merge_rows4<2>(d, a, bb, n, lane); break;
-                default: merge_rows4<3>(d, a, bb, n, lane); break;
-            }
-        } else {
-            for (int i = lane * 4; i < n; i += 128) sts4(d + i, lds4(a + i));
-        }
-    } else {
-        warp_merge(d, a, b ? b + bd : nullptr, n, lane);
-    }
 }
 
 // One merge step of a tile program, all warps of the CTA, warp per op:
@@ -300,9 +252,6 @@ __device__ __forceinline__ void warp_store_col(Out* __restrict__ g, const Acc* s
     for (int i = done + lane; i < n; i += 32) g[i] = static_cast<Out>(s[i]);
 }
 
-__device__ __forceinline__ size_t k1_ops_offset_dev(size_t esz, int max_width, int sr) {
-    return (2 * static_cast<size_t>(max_width) * sr * esz + 15) / 16 * 16;
-}
 
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
