@@ -383,7 +383,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         // K1 rows per tile: every op's window (S + halo) fits the executor's
         // 256-row item pair.
         // K1 rows per tile: the fewest tiles of <= 256 rows, balanced.
-        const int smax = acc_sz == 8 ? 128 : 256;
+        const int smax = acc_sz == 8 ? 128 : env_int("FHT_K1_SMAX", 256, 16, 256);
         const int ntile = (H + smax - 1) / smax;
         int S = ((H + ntile - 1) / ntile + 7) & ~7;
         if (H < S) S = H;
