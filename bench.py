@@ -212,7 +212,10 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        # NCCL across GPUs; FHT_DIST_BACKEND=gloo lets several ranks share one
+        # GPU for functional testing (their kernels never wait on each other).
+        dist.init_process_group(os.environ.get("FHT_DIST_BACKEND", "nccl"), init_method="env://")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     c = workloads.CONFIGS[args.config]

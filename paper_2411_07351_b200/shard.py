@@ -192,20 +192,22 @@ def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: 
         backend.merge(sp, left, 0, right, 0, 0, W, out)
         return out, sp
     mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side)
+    # gloo moves host tensors only: stage the exchange through host memory
+    # (NCCL exchanges device buffers directly over NVLink)
+    host = dist.get_backend(group) == "gloo" and mine.device.type == "cuda"
+    lo, hi = sp.left_for_1 if side == 0 else sp.right_for_0
+    rlo, rhi = sp.right_for_0 if side == 0 else sp.left_for_1
+    send = mine[lo:hi].contiguous()
+    recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
+    send_x, recv_x = (send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)) if host else (send, recv)
     if side == 0:
-        lo, hi = sp.left_for_1
-        send = mine[lo:hi].contiguous()
-        rlo, rhi = sp.right_for_0
-        recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
-        ops = [dist.P2POp(dist.isend, send, peer, group), dist.P2POp(dist.irecv, recv, peer, group)]
+        ops = [dist.P2POp(dist.isend, send_x, peer, group), dist.P2POp(dist.irecv, recv_x, peer, group)]
     else:
-        lo, hi = sp.right_for_0
-        send = mine[lo:hi].contiguous()
-        rlo, rhi = sp.left_for_1
-        recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
-        ops = [dist.P2POp(dist.irecv, recv, peer, group), dist.P2POp(dist.isend, send, peer, group)]
+        ops = [dist.P2POp(dist.irecv, recv_x, peer, group), dist.P2POp(dist.isend, send_x, peer, group)]
     for r in dist.batch_isend_irecv(ops):
         r.wait()
+    if host:
+        recv.copy_(recv_x)
     out = backend.empty_out(sp, mine)
     if side == 0:
         backend.merge(sp, mine, 0, recv, rlo, 0, sp.t_mid, out)

@@ -1,0 +1,89 @@
+"""The multi-rank GPU paths with real kernels: several processes share the one
+GPU of the test box over a gloo process group (their kernels never wait on
+each other; only host-side collectives).  Checks the two-rank root split of a
+quadrant against the single-process transform, and runs bench.py under
+torchrun with 2 ranks (batch shards) and 8 ranks (c5-style root split)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _root_worker(rank, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    torch.cuda.set_device(0)
+    sys.path.insert(0, str(ROOT))
+    from paper_2411_07351_b200 import shard
+
+    rng = np.random.default_rng(9)
+    img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
+    be = shard.GpuRootBackend("tweaked", "f32", "f32")
+    res, sp = shard.root_split_quadrant(img, "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
+    torch.cuda.synchronize()
+    np.save(f"{out}.{rank}.npy", res.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_root_split_two_processes_one_gpu(tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2411_07351_b200 import fht, shard
+
+    out = tmp_path / "rs"
+    mp.spawn(_root_worker, args=(_port(), str(out)), nprocs=2, join=True)
+    rng = np.random.default_rng(9)
+    img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
+    full = fht.Plan(2049, 1500, "tweaked", in_dtype="f32", acc_dtype="f32", quadrants=["vert_pos"])(img[None])
+    ref = full["vert_pos"][0].cpu().numpy()
+    sp = shard.root_split(1500, 2049, "tweaked")
+    a, b = np.load(f"{out}.0.npy"), np.load(f"{out}.1.npy")
+    np.testing.assert_array_equal(a[:, :sp.t_mid], ref[:, :sp.t_mid])
+    np.testing.assert_array_equal(b[:, sp.t_mid:], ref[:, sp.t_mid:])
+
+
+def _torchrun(n, *args):
+    env = dict(os.environ, FHT_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"), "--gpus", str(n),
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_two_ranks_batch_shards():
+    d = _torchrun(2)
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["parallelism"] == "batch-shard x2"
+
+
+def test_bench_eight_ranks_root_split_c5():
+    d = _torchrun(8, "--config", "c5")
+    assert d["n_gpus"] == 8 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["parallelism"] == "root-split x2 per quadrant"
