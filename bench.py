@@ -347,6 +347,18 @@ def run_ours(args):
                 "kernel_ms": {k2: round(v, 4) for k2, v in kernel_share.items()},
                 "kernel_gbs": {names[kd]: round(sum(b for _, b in v) / (sum(m for m, _ in v) * 1e-3) / 1e9, 1)
                                for kd, v in by_kind.items()}}
+    # The north star's per-level design (one HBM pass per tree level) is HBM-
+    # bound; its floor at 100 % of the measured bandwidth is
+    # Q * imgs * n^2 * (e_in + e_acc + 2 e_acc (levels - 1)) / peak (SURVEY §8d,
+    # K = ceil(log2 n) passes).  The fused passes here are shared-memory bound
+    # (low per-pass HBM fraction) yet beat that floor by this factor.
+    levels = int(np.ceil(np.log2(c.n)))
+    imgs_here = c.batch if scaling == "weak" else 1
+    nq_here = len(my_q) if my_q else 0
+    unfused = nq_here * imgs_here * c.n * c.n * (ESZ[c.dtype] + ESZ[c.acc] + 2 * ESZ[c.acc] * (levels - 1))
+    floor_ms = unfused / (peak * 1e9) * 1e3
+    roofline["unfused_hbm_floor_ms"] = round(floor_ms, 4)
+    roofline["vs_unfused_floor"] = round(floor_ms / ms_per_step, 3) if ms_per_step > 0 else None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:

@@ -223,3 +223,29 @@ def test_execute_host_roundtrip():
         ref, _ = oracle.fht2d_quadrants(imgs[bi], 1, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][bi], ref[k])
+
+
+def test_profiled_launch_accounting():
+    """fht_execute_profiled: one record per launch, kinds in launch order and
+    algorithmic bytes that add up to the plan's passes (bench roofline input)."""
+    import ctypes
+
+    from paper_2411_07351_b200._lib import check, lib
+
+    n = 509
+    plan = fht.Plan(n, n, "tweaked", in_dtype="u8", acc_dtype="i32", batch=3)
+    x = torch.zeros((3, n, n), dtype=torch.uint8, device="cuda")
+    out = plan.alloc_outputs()
+    ptrs = (ctypes.c_void_p * 4)(*[out[q].data_ptr() for q in fht.QUADRANTS])
+    ws = plan.workspace()
+    nl = plan.launches
+    ms, kind, by, got = (ctypes.c_float * nl)(), (ctypes.c_int * nl)(), (ctypes.c_double * nl)(), ctypes.c_int()
+    check(lib().fht_execute_profiled(plan._h, ctypes.c_void_p(x.data_ptr()), n * n, ptrs, n * n,
+                                     ctypes.c_void_p(ws.data_ptr()), None, ms, kind, by, nl, ctypes.byref(got)))
+    assert got.value == nl == 3
+    kinds, b = list(kind), list(by)
+    assert kinds == [1, 4, 3]  # generic K1 (remainder block), K1P, root band
+    slots, cells = 3 * 4, n * n
+    assert b[0] + b[1] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
+    assert b[1] == slots * (n // 32) * 32 * n * 5  # the 15 width-32 blocks
+    assert b[2] == slots * cells * 8
