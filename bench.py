@@ -161,7 +161,7 @@ def cpu_baseline(cfg: str, strategy: int, seconds: float, threads: int | None = 
     while True:
         fn(imgs, strategy, threads=threads, mask=mask)
         done += per
-        if time.perf_counter() - t0 >= seconds or done >= 64 * per:
+        if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
     sums = len(quads) * done * c.n * c.n * int(np.ceil(np.log2(c.n)))
