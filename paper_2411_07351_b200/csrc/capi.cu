@@ -371,8 +371,16 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         for (;;) {
             g->sp = SubPlan::build(W, H, strategy, bw, levels, tw);
             bool ok = true;
-            for (const auto& ps : g->sp.passes)
-                ok = ok && pass_rows(ps, H, acc_sz, budget) >= std::min(H, 32);
+            for (const auto& ps : g->sp.passes) {
+                const int rows = pass_rows(ps, H, acc_sz, budget);
+                int tile_ops = 0;
+                for (const auto& t : ps.tiles)
+                    tile_ops = std::max(tile_ops, ps.step_offs[static_cast<size_t>(t.step_beg + t.nsteps)] -
+                                                      ps.step_offs[static_cast<size_t>(t.step_beg)]);
+                const int Lmax = std::min(rows, 256) + ps.max_ext + 20;
+                ok = ok && rows >= std::min(H, 32) &&
+                     fhtb::k2_smem_bytes(acc, ps.max_slots, Lmax, tile_ops) <= 227 * 1024;
+            }
             if (ok) break;
             if (tw == 1) throw FhtError(FHT_ERR_INTERNAL, "fused pass does not fit shared memory");
             tw = std::max(1, tw / 2);
