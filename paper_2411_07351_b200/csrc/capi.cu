@@ -424,6 +424,10 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             g->pass_L.push_back(L2);
         }
         upload(*g);
+        // grid.y carries blocks / tiles: 65535 of them at most
+        bool fits = g->nby <= 65535 && g->nblocks <= 65535;
+        for (const auto& d : g->dt.passes) fits = fits && d.ntiles <= 65535;
+        if (!fits) throw std::invalid_argument("fht2d: working width too large (more than 65535 tiles per pass)");
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
