@@ -145,15 +145,24 @@ def cpu_baseline(cfg: str, strategy: int, seconds: float, threads: int | None = 
     kind = "reference" if oracle.ref_available() else "port"
     quads = c.quadrants
     mask = sum(1 << workloads.ALL_Q.index(q) for q in quads)
+    # Enough images per call that the (image, quadrant) items cover every host
+    # thread (independent steps run side by side for batch-1 configs), capped
+    # by host memory: the reference holds ~4 int64 planes per item in flight.
+    per = max(min(threads, c.batch), -(-threads // len(quads)))
+    try:
+        import psutil
+        fit_items = max(1, int(0.5 * psutil.virtual_memory().available) // (32 * c.n * c.n))
+        threads = min(threads, fit_items)
+        per = max(1, min(per, -(-fit_items // len(quads))))
+    except ImportError:  # pragma: no cover
+        pass
     if c.dtype == "u8":
-        per = max(1, min(threads, c.batch))
         imgs = workloads.make_images(cfg, per)
         proxy = ""
     else:
         # The reference has no float path: time its int64 path on
-        # a same-size integer image ("int64 proxy": same add tree, 8-byte cells).
-        per = 1
-        imgs = np.random.default_rng(0).integers(0, 256, (1, c.n, c.n), dtype=np.uint8)
+        # same-size integer images ("int64 proxy": same add tree, 8-byte cells).
+        imgs = np.random.default_rng(0).integers(0, 256, (per, c.n, c.n), dtype=np.uint8)
         proxy = " (int64 proxy: reference has no float path)"
     fn = oracle.ref_batch_quadrants_u8 if kind == "reference" else oracle.batch_quadrants_u8_port
     t0 = time.perf_counter()

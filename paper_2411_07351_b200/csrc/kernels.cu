@@ -168,6 +168,47 @@ __device__ __forceinline__ void rows_op(uint32_t d, uint32_t a, uint32_t bb, int
     }
 }
 
+__device__ __forceinline__ int lds1u(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts1u(uint32_t a, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+template <class Acc>
+__device__ __forceinline__ int add_bits(int x, int y) {
+    return to_bits<Acc>(from_bits<Acc>(x) + from_bits<Acc>(y));
+}
+
+// The same op with rows interleaved over lanes (lane l owns rows l, l+32,
+// ...): 32 consecutive words are conflict-free at any alignment, so the
+// shifted operand costs one wavefront per 32 rows like the aligned ones
+// (the 4-rows-per-lane form needs a second, 4-way conflicted, b load when
+// the shift is not a multiple of 4).  b is the exact (unaligned) address.
+template <class Acc>
+__device__ __forceinline__ void rows_op_s(uint32_t d, uint32_t a, uint32_t b, int n, int lane) {
+    constexpr int U = 4;  // 128 rows per step (8 measured slower: code size)
+    const uint32_t lo = lane * 4u;
+    int i0 = 0;
+    for (; i0 + 32 * U <= n; i0 += 32 * U) {
+        int x[U], y[U];
+        const uint32_t o = lo + i0 * 4u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            x[u] = lds1u(a + o + 128u * u);
+            y[u] = lds1u(b + o + 128u * u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) sts1u(d + o + 128u * u, add_bits<Acc>(x[u], y[u]));
+    }
+    for (; i0 < n; i0 += 32)
+        if (i0 + lane < n) {
+            const uint32_t o = lo + i0 * 4u;
+            sts1u(d + o, add_bits<Acc>(lds1u(a + o), lds1u(b + o)));
+        }
+}
+
 // K2 window load, 4-byte types: d[i] = col[(start + i) mod H], i < n, with
 // d 16-byte aligned.  The run up to the wrap point is copied with 16-byte
 // loads/stores when `start` is 4-aligned (columns are: ld % 4 == 0); the
@@ -216,7 +257,7 @@ __device__ __forceinline__ void run_step(Acc* sm, int stride, const PassOpDev* _
 
 // 4-byte path with ops baked on the host into 16-byte records of shared
 // byte offsets: {dst, a (+ad), b aligned base | (bd & 3)  (-1: copy), rows}.
-template <class Acc, int NWARPS>
+template <class Acc, int NWARPS, bool SC = false>
 __device__ __forceinline__ void run_step_baked(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane) {
     for (int o = o_beg + warp; o < o_end; o += NWARPS) {
@@ -228,6 +269,10 @@ __device__ __forceinline__ void run_step_baked(uint32_t base, const int4* __rest
             continue;
         }
         const uint32_t bb = base + static_cast<uint32_t>(op.z & ~15);
+        if (SC) {
+            rows_op_s<Acc>(d, a, bb + 4u * static_cast<uint32_t>(op.z & 3), n, lane);
+            continue;
+        }
         switch (op.z & 3) {
             case 0: rows_op<0, Acc>(d, a, bb, n, lane); break;
             case 1: rows_op<1, Acc>(d, a, bb, n, lane); break;
@@ -364,9 +409,10 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
 // (every power-of-two block; all but at most one block of a Tweaked tree).
 // Its ops need no tables: (t0, t1, shift) follow from the column index with
 // a compile-time divisor per level.  512 threads; warp w owns columns w and w + 16 at every
-// level; lanes own 4 consecutive rows (16-byte shared accesses, lanes
-// contiguous: conflict-free).  Leaves live in slots [32, 64), level L
-// writes parity (5 - L) & 1, the block root ends in slots [0, 32).
+// level.  Levels 1-2 run in registers (lanes own 4-row vectors, whose shifted
+// neighbours the level-2 outputs share); levels 3-5 interleave rows over
+// lanes so every shift is conflict-free.  Leaves live in slots [32, 64); the
+// levels alternate parity and the block root ends in slots [32, 64).
 constexpr int kBYW = 32;        // block width
 constexpr int kBYMaxS = 256;    // rows per tile (host guarantees S <= 256)
 constexpr int kBYSR = 300;      // slot stride: >= 256 + 31 + 12, multiple of 4, /4 odd
@@ -394,6 +440,37 @@ __device__ __forceinline__ void by_rows(Acc* __restrict__ d, const Acc* __restri
 #pragma unroll
     for (int c = 0; c < 3; ++c)
         if (lane * 4 + 128 * c < n) sts4(d + 128 * c, add_shift<M, Acc>(av[c], b0[c], M ? b1[c] : b0[c]));
+}
+
+// Levels 3-5, rows interleaved over lanes (lane l owns rows l, l+32, ...):
+// any shift is one conflict-free wavefront per 32 rows (n <= 256 + 31).
+template <class Acc, int L>
+__device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
+    constexpr int w = 1 << L, w0 = w >> 1;
+    constexpr int src = ((7 - L) & 1) * kBYW, dst = ((6 - L) & 1) * kBYW;
+    constexpr int G = (kBYMaxS + kBYW + 31) / 32;  // 9 row groups at most
+    const int n = S + kBYW - w;
+    const uint32_t base = smem_u32(sm) + lane * 4u;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        const int T = warp + h * kWarpsBY;
+        const int tl = T & (w - 1), x0 = T & ~(w - 1);
+        const int t0 = (2 * tl * (w0 - 1) + (w - 1)) / (2 * (w - 1));
+        const int r = tl - t0;
+        const uint32_t d = base + (dst + T) * kBYSR * 4u;
+        const uint32_t a = base + (src + x0 + t0) * kBYSR * 4u;
+        const uint32_t b = base + ((src + x0 + w0 + t0) * kBYSR + r) * 4u;
+        int x[G], y[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            if (32 * u + lane < n) {
+                x[u] = lds1u(a + 128u * u);
+                y[u] = lds1u(b + 128u * u);
+            }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            if (32 * u + lane < n) sts1u(d + 128u * u, add_bits<Acc>(x[u], y[u]));
+    }
 }
 
 template <class Acc, int L, int F = 0>
@@ -539,7 +616,15 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         }
     }
     __syncthreads();
-    if constexpr (V == 2) {
+    if constexpr (V == 3) {
+        by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
+        __syncthreads();
+        by_level_s<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 4>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 5>(sm, S, warp, lane);  // block root -> slots [32, 64)
+    } else if constexpr (V == 2) {
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
         by_level_v0<Acc, 3, 1>(sm, S, warp, lane);
@@ -562,7 +647,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     const int rows_out = min(S, H - s0);
     Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
     const bool al = ((ld | s0) & 3) == 0;
-    const Acc* root = sm + (V == 2 ? kBYW * kBYSR : 0);
+    const Acc* root = sm + (V >= 2 ? kBYW * kBYSR : 0);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int c = warp + h * kWarpsBY;
@@ -620,7 +705,7 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
 }
 
 
-template <class Acc, class Out>
+template <class Acc, class Out, bool SC>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
@@ -666,7 +751,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
         __syncthreads();
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
         if constexpr (sizeof(Acc) == 4)
-            run_step_baked<Acc, kWarps>(sbase, sbops, ob, oe, warp, lane);
+            run_step_baked<Acc, kWarps, SC>(sbase, sbops, ob, oe, warp, lane);
         else
             run_step<Acc, kWarps>(sm, L, sops, ob, oe, S, warp, lane);
     }
@@ -827,7 +912,9 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     }
     if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
-            auto kb = g.k1p_variant == 0 ? k1_by32<In, Acc, 0> : k1_by32<In, Acc, 2>;
+            auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
+                      : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>
+                                           : k1_by32<In, Acc, 3>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
@@ -849,7 +936,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
-        auto k2 = k2_pass<Acc, Out>;
+        auto k2 = g.k2_scalar ? k2_pass<Acc, Out, true> : k2_pass<Acc, Out, false>;
         allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
         k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);

@@ -77,7 +77,9 @@ struct GroupLaunch {
     const int* by_x0;
     cudaStream_t aux_stream;  // plan-owned stream for the concurrent generic-block K1 (may be null)
     cudaEvent_t ev_fork, ev_join;
-    int k1p_variant;    // 2 (default): levels 1-2 in registers; 0: all levels in shared memory
+    int k1p_variant;    // 3 (default): levels 1-2 in registers, 3-5 rows interleaved over lanes;
+                        // 2: levels 3-5 with 4 rows per lane; 0: all levels in shared memory
+    int k2_scalar;      // 1 (default): K2 merge rows interleaved over lanes; 0: 4 rows per lane (int4)
     const ShapeHdr* shapes;
     const int* step_offs;
     const PassOpDev* k1_ops;  // per-shape ops, slots pre-offset by buffer parity

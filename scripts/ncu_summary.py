@@ -20,14 +20,16 @@ def main(rep, top=25):
             print(f"{d['Section Name'][:28]:28s} | {d['Metric Name']} = {d['Metric Value']} {d['Metric Unit']}")
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    if len(rr) > 2:
-        h, units, vals = rr[0], rr[1], rr[2]
+    h, units = (rr[0], rr[1]) if len(rr) > 2 else ([], [])
+    for vals in rr[2:]:
+        kname = dict(zip(h, vals)).get("Kernel Name", "?").split("(")[0]
+        print(f"raw [{kname}]")
         for k, u, v in zip(h, units, vals):
             if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "smsp__inst_executed.sum",
                      "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
                      "sm__sass_inst_executed_op_shared_ld.sum", "sm__sass_inst_executed_op_shared_st.sum",
                      "sm__sass_inst_executed_op_global_ld.sum", "gpu__time_duration.sum"):
-                print(f"raw {k} = {v} {u}")
+                print(f"raw   {k} = {v} {u}")
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     if not src:

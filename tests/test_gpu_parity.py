@@ -126,6 +126,28 @@ def test_float32_small_bit_exact_vs_fp32_tree():
             np.testing.assert_array_equal(out[k][0], ref[k])
 
 
+@pytest.mark.parametrize("k1p,k2", [(0, 0), (2, 0), (2, 1), (3, 0), (3, 1)])
+def test_kernel_variants_bit_exact(monkeypatch, k1p, k2):
+    """Every K1P level variant (0: all levels in shared memory, 2: levels 1-2
+    in registers, 3: + interleaved levels 3-5) and both K2 merge layouts
+    (0: 4 rows per lane, 1: rows interleaved over lanes) against the oracle."""
+    monkeypatch.setenv("FHT_K1P_VARIANT", str(k1p))
+    monkeypatch.setenv("FHT_K2_SCALAR", str(k2))
+    rng = np.random.default_rng(40 + 10 * k1p + k2)
+    for strategy, (h, w) in [(1, (509, 509)), (0, (300, 257)), (1, (1000, 70))]:
+        imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)
+        out, _ = run_plan(imgs, "u8", "i32", strategy)
+        for bi in range(2):
+            ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+            for k in Q:
+                np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} s{strategy} {k}")
+    img = rng.standard_normal((333, 271)).astype(np.float32)
+    out, _ = run_plan(img, "f32", "f32")
+    ref, _ = oracle.fht2d_quadrants(img, 1, dtype=np.float32)
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
+
+
 # --------------------------------------------------- the five configs
 def _cfg_plan(cfg, count=None):
     c = workloads.CONFIGS[cfg]
