@@ -790,7 +790,9 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane + 32 * h;
                         if (c >= nc) continue;
-                        const int4 v4 = lds4(sm + (size_t)(h ? sl1 : sl0) * L + i);
+                        // one 16-byte read (the compiler splits a C++ int4 load
+                        // it cannot prove aligned into two conflicting LDS.64)
+                        const int4 v4 = lds4u(smem_u32(sm + (size_t)(h ? sl1 : sl0) * L + i));
                         const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
