@@ -98,6 +98,7 @@ struct Group {
     int ld = 0, S = 0, sr = 0, nbuf = 0;
     int nblocks = 0, nby = 0;
     bool use_by32 = false;
+    bool pairs = false;  // K2 runs the level-pair programs (4-byte accumulators)
     std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
     size_t slot_bytes = 0;
 };
@@ -109,6 +110,25 @@ constexpr int kHostStreams = 3;
 int env_int(const char* name, int def, int lo, int hi) {
     if (const char* e = std::getenv(name)) return std::max(lo, std::min(hi, std::atoi(e)));
     return def;
+}
+
+// The tile program K2 executes for a pass: one level per step (PassOp), or
+// the level-pair program (PassOpN, plan.hpp) -- same tiles and loads.
+struct PassProgram {
+    const std::vector<fhtb::PassTile>& tiles;
+    const std::vector<int>& step_offs;
+    const std::vector<fhtb::PassStore>& stores;
+    int max_slots;
+    int max_tile_ops() const {
+        int m = 0;
+        for (const auto& t : tiles)
+            m = std::max(m, step_offs[static_cast<size_t>(t.step_beg + t.nsteps)] - step_offs[static_cast<size_t>(t.step_beg)]);
+        return m;
+    }
+};
+PassProgram program(const fhtb::FusedPass& ps, bool pairs) {
+    if (pairs) return {ps.ptiles, ps.pstep_offs, ps.pstores, ps.pmax_slots};
+    return {ps.tiles, ps.step_offs, ps.stores, ps.max_slots};
 }
 
 
@@ -246,21 +266,35 @@ void upload(Group& g) {
     for (const auto& ps : sp.passes) {
         static_assert(sizeof(fhtb::PassTile) == sizeof(fhtb::PassTileDev), "tile layout");
         static_assert(sizeof(fhtb::PassOp) == sizeof(fhtb::PassOpDev), "op layout");
+        const PassProgram pr = program(ps, g.pairs);
         PassOff o{};
-        o.tiles = put(ps.tiles.data(), ps.tiles.size() * sizeof(fhtb::PassTile));
+        o.tiles = put(pr.tiles.data(), pr.tiles.size() * sizeof(fhtb::PassTile));
         std::vector<int4> loads;
         for (const auto& l : ps.loads) loads.push_back(make_int4(l.gcol, l.slot, l.off, l.ext));
         o.loads = put(loads.data(), loads.size() * sizeof(int4));
-        o.steps = put(ps.step_offs.data(), ps.step_offs.size() * sizeof(int));
+        o.steps = put(pr.step_offs.data(), pr.step_offs.size() * sizeof(int));
         o.ops = put(ps.ops.data(), ps.ops.size() * sizeof(fhtb::PassOp));
         std::vector<int2> stores;
-        for (const auto& st : ps.stores) stores.push_back(make_int2(st.slot, st.gcol));
+        for (const auto& st : pr.stores) stores.push_back(make_int2(st.slot, st.gcol));
         o.stores = put(stores.data(), stores.size() * sizeof(int2));
         // ops baked into shared byte offsets for the 4-byte kernel path
         {
             const int64_t L = g.pass_L[o_passes.size()], S = g.pass_S[o_passes.size()];
             std::vector<int4> bops;
+            if (g.pairs) {  // 2 records per op: {dst, rows, nterms, term0}, {term1, term2, term3, split}
+                for (const auto& op : ps.pops) {
+                    int64_t t[4] = {0, 0, 0, 0};
+                    for (int k = 0; k < op.nterms; ++k) t[k] = (op.term[k].slot * L + op.term[k].off) * 4;
+                    const int64_t d = op.dst * L * 4;
+                    if (d > INT32_MAX || *std::max_element(t, t + 4) > INT32_MAX)
+                        throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
+                    bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(S + op.ext), op.nterms,
+                                             static_cast<int>(t[0])));
+                    bops.push_back(make_int4(static_cast<int>(t[1]), static_cast<int>(t[2]), static_cast<int>(t[3]), op.split));
+                }
+            }
             for (const auto& op : ps.ops) {
+                if (g.pairs) break;
                 const int64_t d = op.dst * L * 4, a = (op.a * L + op.ad) * 4;
                 const int64_t b = op.b < 0 ? -1 : ((op.b * L + (op.bd & ~3)) * 4) | (op.bd & 3);
                 if (d > INT32_MAX || a > INT32_MAX || b > INT32_MAX) throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
@@ -292,12 +326,11 @@ void upload(Group& g) {
         d.bops = reinterpret_cast<const int4*>(base + o.bops);
         d.S = g.pass_S[i];
         d.L = g.pass_L[i];
-        d.ntiles = static_cast<int>(sp.passes[i].tiles.size());
-        d.max_slots = sp.passes[i].max_slots;
-        d.max_tile_ops = 0;
-        for (const auto& t : sp.passes[i].tiles)
-            d.max_tile_ops = std::max(d.max_tile_ops, sp.passes[i].step_offs[static_cast<size_t>(t.step_beg + t.nsteps)] -
-                                                          sp.passes[i].step_offs[static_cast<size_t>(t.step_beg)]);
+        const PassProgram pr = program(sp.passes[i], g.pairs);
+        d.ntiles = static_cast<int>(pr.tiles.size());
+        d.max_slots = pr.max_slots;
+        d.max_tile_ops = pr.max_tile_ops();
+        d.pairs = g.pairs ? 1 : 0;
         g.dt.passes.push_back(d);
     }
 }
@@ -305,8 +338,8 @@ void upload(Group& g) {
 
 // Rows per K2 row tile for a pass: as many as fit `budget` bytes of shared
 // memory (max_slots slots of S + max_ext rows), capped at H; multiples of 32.
-int pass_rows(const fhtb::FusedPass& ps, int H, size_t esz, size_t budget) {
-    const long cap = static_cast<long>(budget / (esz * static_cast<size_t>(std::max(1, ps.max_slots)))) - ps.max_ext - 20;
+int pass_rows(const fhtb::FusedPass& ps, int max_slots, int H, size_t esz, size_t budget) {
+    const long cap = static_cast<long>(budget / (esz * static_cast<size_t>(std::max(1, max_slots)))) - ps.max_ext - 20;
     if (cap >= H) return H;
     if (cap < 32) return static_cast<int>(std::max(0L, cap));
     return static_cast<int>(cap / 32 * 32);
@@ -368,18 +401,16 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 105, 16, 220)) * 1024;
         const int levels = env_int("FHT_PASS_LEVELS", 4, 1, 8);
         int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
+        g->pairs = acc_sz == 4 && env_int("FHT_K2_PAIRS", 1, 0, 1) == 1;
         for (;;) {
             g->sp = SubPlan::build(W, H, strategy, bw, levels, tw);
             bool ok = true;
             for (const auto& ps : g->sp.passes) {
-                const int rows = pass_rows(ps, H, acc_sz, budget);
-                int tile_ops = 0;
-                for (const auto& t : ps.tiles)
-                    tile_ops = std::max(tile_ops, ps.step_offs[static_cast<size_t>(t.step_beg + t.nsteps)] -
-                                                      ps.step_offs[static_cast<size_t>(t.step_beg)]);
+                const PassProgram pr = program(ps, g->pairs);
+                const int rows = pass_rows(ps, pr.max_slots, H, acc_sz, budget);
                 const int Lmax = std::min(rows, 256) + ps.max_ext + 20;
                 ok = ok && rows >= std::min(H, 32) &&
-                     fhtb::k2_smem_bytes(acc, ps.max_slots, Lmax, tile_ops) <= 227 * 1024;
+                     fhtb::k2_smem_bytes(acc, pr.max_slots, Lmax, pr.max_tile_ops()) <= 227 * 1024;
             }
             if (ok) break;
             if (tw == 1) throw FhtError(FHT_ERR_INTERNAL, "fused pass does not fit shared memory");
@@ -409,7 +440,8 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         g->use_by32 = acc_sz == 4 && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
         g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
         for (size_t i = 0; i < g->sp.passes.size(); ++i) {
-            int S2 = std::min(256, pass_rows(g->sp.passes[i], H, acc_sz, budget));
+            int S2 = std::min(256, pass_rows(g->sp.passes[i], program(g->sp.passes[i], g->pairs).max_slots, H, acc_sz,
+                                             budget));
             {  // balance the row tiles
                 const int nt = (H + S2 - 1) / std::max(1, S2);
                 S2 = std::min(S2, ((H + nt - 1) / nt + 7) & ~7);
@@ -488,6 +520,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.by_x0 = g.dt.by_x0;
             L.k1p_variant = env_int("FHT_K1P_VARIANT", 3, 0, 3);  // see GroupLaunch
             L.k2_scalar = env_int("FHT_K2_SCALAR", 1, 0, 1);
+            L.k2_bulk = env_int("FHT_K2_BULK", 0, 0, 1);
             L.aux_stream = env_int("FHT_K1_OVERLAP", 1, 0, 1) ? p->aux : nullptr;
             L.ev_fork = p->ev_fork;
             L.ev_join = p->ev_join;
@@ -987,7 +1020,27 @@ int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_leve
             o << "],\"stores\":[";
             for (size_t k = 0; k < ps.stores.size(); ++k)
                 o << (k ? "," : "") << "[" << ps.stores[k].slot << "," << ps.stores[k].gcol << "]";
-            o << "]}";
+            // the level-pair program (ops: [dst, ext, [[slot, off], ...]])
+            o << "],\"pairs\":{\"max_slots\":" << ps.pmax_slots << ",\"tiles\":[";
+            for (size_t k = 0; k < ps.ptiles.size(); ++k) {
+                const auto& t = ps.ptiles[k];
+                o << (k ? "," : "") << "[" << t.load_beg << "," << t.load_cnt << "," << t.step_beg << "," << t.nsteps << ","
+                  << t.store_beg << "," << t.store_cnt << "," << t.nslots << "," << t.max_ext << "]";
+            }
+            o << "],\"step_offs\":[";
+            for (size_t k = 0; k < ps.pstep_offs.size(); ++k) o << (k ? "," : "") << ps.pstep_offs[k];
+            o << "],\"ops\":[";
+            for (size_t k = 0; k < ps.pops.size(); ++k) {
+                const auto& op = ps.pops[k];
+                o << (k ? "," : "") << "[" << op.dst << "," << op.ext << ",[";
+                for (int j = 0; j < op.nterms; ++j)
+                    o << (j ? "," : "") << "[" << op.term[j].slot << "," << op.term[j].off << "]";
+                o << "]," << op.split << "]";
+            }
+            o << "],\"stores\":[";
+            for (size_t k = 0; k < ps.pstores.size(); ++k)
+                o << (k ? "," : "") << "[" << ps.pstores[k].slot << "," << ps.pstores[k].gcol << "]";
+            o << "]}}";
         }
         o << "]}";
         const std::string s = o.str();

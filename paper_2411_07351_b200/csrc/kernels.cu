@@ -209,6 +209,62 @@ __device__ __forceinline__ void rows_op_s(uint32_t d, uint32_t a, uint32_t b, in
         }
 }
 
+// A level-pair op (plan.hpp PassOpN): d[i] = sum of K shifted windows,
+// added in the tree's order -- (first child's terms) + (second child's).
+template <class Acc, int K, int SPLIT>
+__device__ __forceinline__ int sum_terms(const int (&v)[4]) {
+    if constexpr (K == 2) return add_bits<Acc>(v[0], v[1]);
+    if constexpr (K == 3 && SPLIT == 2) return add_bits<Acc>(add_bits<Acc>(v[0], v[1]), v[2]);
+    if constexpr (K == 3) return add_bits<Acc>(v[0], add_bits<Acc>(v[1], v[2]));
+    return add_bits<Acc>(add_bits<Acc>(v[0], v[1]), add_bits<Acc>(v[2], v[3]));
+}
+template <class Acc, int K, int SPLIT>
+__device__ __forceinline__ void rows_op_terms(uint32_t d, const uint32_t (&t)[4], int n, int lane) {
+    constexpr int U = 4;
+    const uint32_t lo = lane * 4u;
+    int i0 = 0;
+    for (; i0 + 32 * U <= n; i0 += 32 * U) {
+        int v[U][4];
+        const uint32_t o = lo + i0 * 4u;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) sts1u(d + o + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
+    }
+    for (; i0 < n; i0 += 32)
+        if (i0 + lane < n) {
+            const uint32_t o = lo + i0 * 4u;
+            int v[4];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + o);
+            sts1u(d + o, sum_terms<Acc, K, SPLIT>(v));
+        }
+}
+
+template <class Acc, int NWARPS>
+__device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
+                                               int warp, int lane) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 h = ops[2 * o], q = ops[2 * o + 1];
+        const uint32_t d = base + static_cast<uint32_t>(h.x);
+        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        const int n = h.y;
+        if (h.z == 4) {
+            rows_op_terms<Acc, 4, 2>(d, t, n, lane);
+        } else if (h.z == 2) {
+            rows_op_terms<Acc, 2, 1>(d, t, n, lane);
+        } else if (h.z == 3) {
+            if (q.w == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
+            else rows_op_terms<Acc, 3, 1>(d, t, n, lane);
+        } else {  // a single term: copy
+            for (int i = lane; i < n; i += 32) sts1u(d + 4u * i, lds1u(t[0] + 4u * i));
+        }
+    }
+}
+
 // K2 window load, 4-byte types: d[i] = col[(start + i) mod H], i < n, with
 // d 16-byte aligned.  The run up to the wrap point is copied with 16-byte
 // loads/stores when `start` is 4-aligned (columns are: ld % 4 == 0); the
@@ -444,10 +500,10 @@ __device__ __forceinline__ void by_rows(Acc* __restrict__ d, const Acc* __restri
 
 // Levels 3-5, rows interleaved over lanes (lane l owns rows l, l+32, ...):
 // any shift is one conflict-free wavefront per 32 rows (n <= 256 + 31).
-template <class Acc, int L>
+template <class Acc, int L, int F = 0>
 __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
     constexpr int w = 1 << L, w0 = w >> 1;
-    constexpr int src = ((7 - L) & 1) * kBYW, dst = ((6 - L) & 1) * kBYW;
+    constexpr int src = ((7 - L + F) & 1) * kBYW, dst = ((6 - L + F) & 1) * kBYW;
     constexpr int G = (kBYMaxS + kBYW + 31) / 32;  // 9 row groups at most
     const int n = S + kBYW - w;
     const uint32_t base = smem_u32(sm) + lane * 4u;
@@ -676,13 +732,42 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// TMA bulk copies (cp.async.bulk, no LSU work) completing on an mbarrier.
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// one lane: dst/src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    mbar_expect_tx(bar, bytes);  // before the copy that completes it (tx count never negative)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // Issue the window copies of one K2 tile (all warps; warp per window).  The
 // warp's window records are fetched with one load per lane up front and
 // broadcast with shuffles, so no descriptor load sits on the issue path.
 template <class Acc>
 __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileDev& tile, const Acc* __restrict__ in,
                                               uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
-                                              int lane) {
+                                              int lane, uint32_t bar) {
     constexpr int kW = kThreads2 / 32;
     for (int base = 0; base < tile.load_cnt; base += 32 * kW) {
         const int mine = base + warp + kW * lane;
@@ -697,15 +782,36 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
             const Acc* col = in + (size_t)w.x * ld;
             const uint32_t d = stage + static_cast<uint32_t>(w.y) * L * 4u;
             const int start = wrap_any(s0 + w.z, H), n = S + w.w;
-            const int run = (start & 3) ? 0 : (min(n, H - start) & ~3);
-            for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
-            for (int i = run + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(start + i, H));
+            // rows [start, H) then (past the wrap point) [0, n - (H - start)):
+            // 16-byte copies while both sides are 16-byte aligned, 4-byte after
+            const int na = min(n, H - start);
+            const int run = (start & 3) ? 0 : (na & ~3);
+            if (bar) {  // aligned runs by the TMA engine, the rest 4-byte
+                if (lane == 0 && run > 0) bulk_copy(d, col + start, run * 4u, bar);
+            } else {
+                for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
+            }
+            for (int i = run + lane; i < na; i += 32) cp_async4(d + 4u * i, col + start + i);
+            if (n - na <= H) {
+                const Acc* cb = col - na;  // rows past the wrap point: col[i - na]
+                int i0 = na;
+                if (bar && (na & 3) == 0) {
+                    const int nb = (n - na) & ~3;
+                    if (lane == 0 && nb > 0) bulk_copy(d + 4u * na, col, nb * 4u, bar);
+                    i0 += nb;
+                }
+                for (int i = i0 + lane; i < n; i += 32) cp_async4(d + 4u * i, cb + i);
+            } else {  // a window longer than the column (tiny H): wraps again
+                for (int i = na + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(i - na, H));
+            }
         }
     }
 }
 
 
-template <class Acc, class Out, bool SC>
+// MODE 0: one level per step, 4 rows per lane; 1: rows interleaved over
+// lanes; 2: level-pair programs (4-byte accumulators only).
+template <class Acc, class Out, int MODE>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
@@ -725,7 +831,9 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     int* ssteps = reinterpret_cast<int*>(sops + ps.max_tile_ops);  // the tile's step offsets (after the ops)
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid];
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
-    if constexpr (sizeof(Acc) == 4) {
+    if constexpr (MODE == 2) {
+        for (int k = tid; k < 2 * nops; k += kThreads2) sbops[k] = ps.bops[2 * op0 + k];
+    } else if constexpr (sizeof(Acc) == 4) {
         for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
     } else {
         for (int k = tid; k < nops * 2; k += kThreads2)
@@ -735,9 +843,20 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     if constexpr (sizeof(Acc) == 4) {
         // cp.async: every window copy of the tile in flight at once, no
         // register staging (16-byte copies before the wrap point, 4-byte after)
-        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane);
+        // the mbarrier sits in the gap after the slots; one arrival per warp
+        const uint32_t bar = ps.bulk ? smem_u32(sm + (size_t)ps.max_slots * L + 8) : 0u;
+        if (bar) {
+            if (tid == 0) mbar_init(bar, kWarps);
+            __syncthreads();
+        }
+        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane, bar);
         cp_async_commit();
+        if (bar) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar);
+        }
         cp_async_wait0();
+        if (bar) mbar_wait(bar, 0);
     } else {
         for (int l = warp; l < tile.load_cnt; l += kWarps) {
             const int4 ld4 = ps.loads[tile.load_beg + l];
@@ -750,8 +869,10 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
-        if constexpr (sizeof(Acc) == 4)
-            run_step_baked<Acc, kWarps, SC>(sbase, sbops, ob, oe, warp, lane);
+        if constexpr (MODE == 2)
+            run_step_terms<Acc, kWarps>(sbase, sbops, ob, oe, warp, lane);
+        else if constexpr (sizeof(Acc) == 4)
+            run_step_baked<Acc, kWarps, MODE == 1>(sbase, sbops, ob, oe, warp, lane);
         else
             run_step<Acc, kWarps>(sm, L, sops, ob, oe, S, warp, lane);
     }
@@ -938,10 +1059,16 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
-        auto k2 = g.k2_scalar ? k2_pass<Acc, Out, true> : k2_pass<Acc, Out, false>;
+        auto k2 = k2_pass<Acc, Out, 0>;
+        if constexpr (sizeof(Acc) == 4) {
+            if (ps.pairs) k2 = k2_pass<Acc, Out, 2>;
+            else if (g.k2_scalar) k2 = k2_pass<Acc, Out, 1>;
+        }
+        PassDev pd = ps;
+        pd.bulk = g.k2_bulk;
         allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
-        k2<<<g2, kThreads2, smem2, st>>>(ps, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
+        k2<<<g2, kThreads2, smem2, st>>>(pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
         ++launches;
         if (hook) hook(ctx, final_pass ? 3 : 2);
     }

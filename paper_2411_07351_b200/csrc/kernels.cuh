@@ -54,6 +54,8 @@ struct PassDev {
     int L;       // smem row capacity of a slot (>= S + max_ext, odd)
     int max_slots;
     int max_tile_ops;  // most merge ops in one tile (staged in shared memory)
+    int bulk;          // window runs by TMA bulk copies (set per launch)
+    int pairs;         // the tables are level-pair programs (bops: 2 records per op)
 };
 
 struct GroupLaunch {
@@ -79,6 +81,7 @@ struct GroupLaunch {
     cudaEvent_t ev_fork, ev_join;
     int k1p_variant;    // 3 (default): levels 1-2 in registers, 3-5 rows interleaved over lanes;
                         // 2: levels 3-5 with 4 rows per lane; 0: all levels in shared memory
+    int k2_bulk;        // K2 aligned window runs by cp.async.bulk (TMA) instead of 16-byte cp.async
     int k2_scalar;      // 1 (default): K2 merge rows interleaved over lanes; 0: 4 rows per lane (int4)
     const ShapeHdr* shapes;
     const int* step_offs;

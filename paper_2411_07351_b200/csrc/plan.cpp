@@ -299,6 +299,89 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
     ps.max_slots = std::max(ps.max_slots, next_slot);
     ps.max_ext = std::max(ps.max_ext, max_ext);
     ps.tiles.push_back(tile);
+
+    // ---- the level-pair program of the same tile (steps 2g, 2g+1 fused)
+    PassTile pt = tile;
+    pt.step_beg = static_cast<int>(ps.pstep_offs.size());
+    pt.nsteps = (hx + 1) / 2;
+    pt.store_beg = static_cast<int>(ps.pstores.size());
+    std::vector<std::vector<int>> pslot(nodes.size());
+    for (int n : order) pslot[static_cast<size_t>(n)].assign(static_cast<size_t>(nodes[static_cast<size_t>(n)].w), -1);
+    for (int n : order)
+        if (front[static_cast<size_t>(n)])
+            for (int t = 0; t < nodes[static_cast<size_t>(n)].w; ++t)
+                pslot[static_cast<size_t>(n)][static_cast<size_t>(t)] = ent[static_cast<size_t>(n)][static_cast<size_t>(t)].slot;
+    int pnext = tile.load_cnt;
+    std::vector<int> pfree;
+    std::vector<std::pair<int, int>> plive;
+    for (int n : order)
+        if (front[static_cast<size_t>(n)])
+            for (int t = 0; t < nodes[static_cast<size_t>(n)].w; ++t)
+                if (ent[static_cast<size_t>(n)][static_cast<size_t>(t)].seen) plive.push_back({n, t});
+    auto step_of = [&](int n) { return front[static_cast<size_t>(n)] ? -1 : height[static_cast<size_t>(n)] - 1; };
+    for (int gs = 0; gs < hx; gs += 2) {
+        const int ge = std::min(hx, gs + 2) - 1;
+        ps.pstep_offs.push_back(static_cast<int>(ps.pops.size()));
+        for (int j = gs; j <= ge; ++j)
+            for (int n : step_nodes[static_cast<size_t>(j)]) {
+                const Node& nd = nodes[static_cast<size_t>(n)];
+                for (int t = 0; t < nd.w; ++t) {
+                    const Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+                    if (!e.seen) continue;
+                    // stored, or read after this step: materialise; else the
+                    // next level of the pair sums its terms itself
+                    if (n != X && e.last_use <= ge) continue;
+                    PassOpN op{};
+                    op.ext = e.hi - e.lo;
+                    // terms of (node, col) at a row shift: a child made earlier in
+                    // this step is expanded into its own two terms
+                    auto add_terms = [&](auto&& self, int m, int c, int shift, bool expand) -> void {
+                        if (!expand) {
+                            const Entry& ce = ent[static_cast<size_t>(m)][static_cast<size_t>(c)];
+                            const int slot = pslot[static_cast<size_t>(m)][static_cast<size_t>(c)];
+                            const int off = e.lo + shift - ce.lo;
+                            if (op.nterms >= 4 || slot < 0 || off < 0 || off + op.ext > ce.hi - ce.lo)
+                                throw std::logic_error("level-pair program derivation failed");
+                            op.term[op.nterms++] = {slot, off};
+                            return;
+                        }
+                        const Node& md = nodes[static_cast<size_t>(m)];
+                        const int w = md.w, w0 = nodes[static_cast<size_t>(md.child[0])].w, w1 = w - w0;
+                        const int t0 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(c) * (w0 - 1), w - 1));
+                        const int t1 = static_cast<int>(round_half_up_ratio(static_cast<int64_t>(c) * (w1 - 1), w - 1));
+                        const int r = (c - t1) % H;
+                        self(self, md.child[0], t0, shift, step_of(md.child[0]) >= gs && m == n);
+                        if (m == n) op.split = op.nterms;  // terms of the first child: the add order
+                        self(self, md.child[1], t1, shift + r, step_of(md.child[1]) >= gs && m == n);
+                    };
+                    add_terms(add_terms, n, t, 0, true);
+                    if (pfree.empty()) {
+                        op.dst = pnext++;
+                    } else {
+                        op.dst = pfree.back();
+                        pfree.pop_back();
+                    }
+                    pslot[static_cast<size_t>(n)][static_cast<size_t>(t)] = op.dst;
+                    ps.pops.push_back(op);
+                    plive.push_back({n, t});
+                }
+            }
+        // free what was last read in this step (reusable from the next step)
+        std::vector<std::pair<int, int>> keep;
+        for (auto [n, t] : plive) {
+            const Entry& e = ent[static_cast<size_t>(n)][static_cast<size_t>(t)];
+            if (n != X && e.last_use <= ge)
+                pfree.push_back(pslot[static_cast<size_t>(n)][static_cast<size_t>(t)]);
+            else
+                keep.push_back({n, t});
+        }
+        plive.swap(keep);
+    }
+    ps.pstep_offs.push_back(static_cast<int>(ps.pops.size()));
+    for (int t = ta; t < tb; ++t) ps.pstores.push_back({pslot[static_cast<size_t>(X)][static_cast<size_t>(t)], xn.x0 + t});
+    pt.nslots = pnext;
+    ps.pmax_slots = std::max(ps.pmax_slots, pnext);
+    ps.ptiles.push_back(pt);
 }
 
 }  // namespace

@@ -81,6 +81,17 @@ struct PassStore {
 struct PassTile {
     int load_beg, load_cnt, step_beg, nsteps, store_beg, store_cnt, nslots, max_ext;
 };
+// An op of a level-pair program: dst[i] = sum_k slot_k[i + off_k], i < S + ext
+// (nterms = 2: one level; 3 or 4: two levels, the intermediate column summed
+// in registers instead of stored).
+struct PassTerm {
+    int slot, off;
+};
+struct PassOpN {
+    int dst, ext, nterms;
+    PassTerm term[4];
+    int split;  // terms [0, split) form the first child: sum = (first) + (rest), the tree's add order
+};
 struct FusedPass {
     int levels = 0;  // tree levels this pass advances (max over its tiles)
     std::vector<PassTile> tiles;
@@ -90,6 +101,14 @@ struct FusedPass {
     std::vector<PassStore> stores;
     int max_slots = 0, max_ext = 0, tile_width = 0;
     int64_t loaded_cells = 0;  // sum over tiles of loaded window cells at S = 0 (per-row-tile overhead)
+    // The same tiles as a level-pair program (same loads and slots 0..load_cnt):
+    // each step advances two levels; an intermediate column read only by the
+    // next level is never materialised.  Slots are freed at step boundaries.
+    std::vector<PassTile> ptiles;
+    std::vector<int> pstep_offs;
+    std::vector<PassOpN> pops;
+    std::vector<PassStore> pstores;
+    int pmax_slots = 0;
 };
 
 // The schedule for one working orientation (width W = number of slopes,

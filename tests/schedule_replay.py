@@ -8,9 +8,10 @@ oracle before any CUDA runs.  Test helper only.
 import numpy as np
 
 
-def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None) -> np.ndarray:
+def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None, pairs: bool = False) -> np.ndarray:
     """cols[x, y] = working column x, row y (W x H).  Returns OUT_0[t, s].
-    S = K1 row tile; pass_S = K2 row tile (default: H)."""
+    S = K1 row tile; pass_S = K2 row tile (default: H); pairs: run the
+    level-pair programs (the 4-byte K2 path) instead of one level per step."""
     W, H = cols.shape
     S = min(S, H)
     PS = min(pass_S or H, H)
@@ -37,6 +38,7 @@ def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None) -> 
     passes = sched["passes"]
     result = np.zeros((W, H), cols.dtype)
     for p, ps in enumerate(passes):
+        ps = _as_unit_program(ps) if pairs else _terms_program(ps)
         src = bufs[p & 1]
         dst = result if p == len(passes) - 1 else bufs[(p + 1) & 1]
         written = np.zeros(W, bool)
@@ -47,14 +49,17 @@ def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None) -> 
                     sm[slot] = src[gcol][(s0 + off + np.arange(PS + ext)) % H]
                 for k in range(nsteps):
                     step = ps["ops"][ps["step_offs"][sb + k]:ps["step_offs"][sb + k + 1]]
-                    reads = {o[1] for o in step} | {o[2] for o in step if o[2] >= 0}
+                    reads = {slot for o in step for slot, _ in o[2]}
                     writes = [o[0] for o in step]
                     assert len(set(writes)) == len(writes) and not (set(writes) & reads), "slot reuse within a step"
                     new = {}
-                    for d, a, b, ad, bd, ext in step:
+                    for d, ext, terms, *_ in step:
                         n = PS + ext
-                        assert ad + n <= len(sm[a]) and (b < 0 or bd + n <= len(sm[b])), "window overrun"
-                        new[d] = sm[a][ad:ad + n] + sm[b][bd:bd + n] if b >= 0 else sm[a][ad:ad + n].copy()
+                        assert all(off >= 0 and off + n <= len(sm[slot]) for slot, off in terms), "window overrun"
+                        acc = sm[terms[0][0]][terms[0][1]:terms[0][1] + n].copy()
+                        for slot, off in terms[1:]:
+                            acc = acc + sm[slot][off:off + n]
+                        new[d] = acc
                     assert max(writes, default=-1) < nslots
                     sm.update(new)
                 m = min(PS, H - s0)
@@ -63,6 +68,16 @@ def replay(cols: np.ndarray, sched: dict, S: int, pass_S: int | None = None) -> 
                     written[gcol] = True
         assert written.all(), "a pass did not write every column"
     return result
+
+
+def _as_unit_program(ps: dict) -> dict:
+    return dict(ps["pairs"], loads=ps["loads"])
+
+
+def _terms_program(ps: dict) -> dict:
+    """One-level ops [dst, a, b, ad, bd, ext] as [dst, ext, terms]."""
+    ops = [[d, ext, [[a, ad]] + ([[b, bd]] if b >= 0 else [])] for d, a, b, ad, bd, ext in ps["ops"]]
+    return dict(ps, ops=ops)
 
 
 def working_cols(img: np.ndarray, q: int) -> np.ndarray:

@@ -126,13 +126,18 @@ def test_float32_small_bit_exact_vs_fp32_tree():
             np.testing.assert_array_equal(out[k][0], ref[k])
 
 
-@pytest.mark.parametrize("k1p,k2", [(0, 0), (2, 0), (2, 1), (3, 0), (3, 1)])
-def test_kernel_variants_bit_exact(monkeypatch, k1p, k2):
+@pytest.mark.parametrize("k1p,k2,pairs,bulk", [(0, 0, 0, 0), (2, 0, 0, 0), (2, 1, 0, 0), (3, 0, 0, 1), (3, 1, 0, 0),
+                                              (3, 1, 1, 0), (3, 1, 1, 1)])
+def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk):
     """Every K1P level variant (0: all levels in shared memory, 2: levels 1-2
-    in registers, 3: + interleaved levels 3-5) and both K2 merge layouts
-    (0: 4 rows per lane, 1: rows interleaved over lanes) against the oracle."""
+    in registers, 3: + interleaved levels 3-5), both one-level K2 merge
+    layouts (0: 4 rows per lane, 1: rows interleaved over lanes), the
+    level-pair K2 programs and the TMA bulk window loads, against the oracle
+    (the f32 case bit-exact: pairs keep the tree's add order)."""
     monkeypatch.setenv("FHT_K1P_VARIANT", str(k1p))
     monkeypatch.setenv("FHT_K2_SCALAR", str(k2))
+    monkeypatch.setenv("FHT_K2_PAIRS", str(pairs))
+    monkeypatch.setenv("FHT_K2_BULK", str(bulk))
     rng = np.random.default_rng(40 + 10 * k1p + k2)
     for strategy, (h, w) in [(1, (509, 509)), (0, (300, 257)), (1, (1000, 70))]:
         imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)

@@ -13,10 +13,11 @@ def _check(h, w, strategy, bw, S, rng, q=0, lo=-1000, hi=1000, levels=4, tw=32, 
     cols = working_cols(img, q)
     W, H = cols.shape
     sched = fht.schedule(W, H, strategy, bw, levels, tw)
-    out = replay(cols, sched, S, pass_S)
     quads, _ = oracle.fht2d_quadrants(img, strategy)
     expect = quads[oracle.QUADRANTS[q]]  # [s, t]
-    np.testing.assert_array_equal(out.T, expect)
+    for pairs in (False, True):  # one level per step (int64 K2) and level pairs (4-byte K2)
+        out = replay(cols, sched, S, pass_S, pairs=pairs)
+        np.testing.assert_array_equal(out.T, expect, err_msg=f"pairs={pairs}")
     assert sched["additions"] == oracle.count_additions_tree(W, H, strategy)
 
 
