@@ -99,6 +99,9 @@ struct Group {
     int nblocks = 0, nby = 0;
     bool use_by32 = false;
     bool pairs = false;  // K2 runs the level-pair programs (4-byte accumulators)
+    // u8 staging for K1P (kernels.cuh GroupLaunch::stage): bytes per image,
+    // column pitch, offsets of the T / P column sets (-1: not staged)
+    long long stage_img = 0, stage_pitch = 0, stage_t = -1, stage_p = -1;
     std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
     size_t slot_bytes = 0;
 };
@@ -140,6 +143,7 @@ struct fht_plan_s {
     int chunk = 1;
     int num_sms = 148;
     size_t ws_bytes = 0;
+    size_t slot_bytes_img = 0, stage_bytes_img = 0;  // workspace per image: slot buffers, then u8 staging
     int launches = 0;
     uint64_t additions = 0;
     std::mutex host_mu;
@@ -438,6 +442,21 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         }
         g->nbuf = g->sp.root_is_block ? 0 : (g->sp.passes.size() > 1 ? 2 : 1);
         g->use_by32 = acc_sz == 4 && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
+        // staging pays off once the batch is large (its launch costs a few
+        // microseconds: a loss for one small image); FHT_K1_STAGE=0/1 forces it
+        const int stage_env = env_int("FHT_K1_STAGE", -1, -1, 1);
+        const bool stage_on = stage_env < 0 ? static_cast<int64_t>(batch) * w * h >= (int64_t(8) << 20) : stage_env == 1;
+        if (in == FHT_U8 && g->use_by32 && stage_on) {
+            // columns of ntile * S + 31 rows (+ the last 4-byte word), 16-byte aligned
+            bool need_t = false, need_p = false;
+            for (int k = 0; k < g->qs.n; ++k) (codes[static_cast<size_t>(k)] < 2 ? need_t : need_p) = true;
+            const long long ntile = (H + S - 1) / S;
+            g->stage_pitch = (ntile * S + 36 + 15) / 16 * 16;
+            const long long set = static_cast<long long>(W) * g->stage_pitch;
+            g->stage_t = need_t ? 0 : -1;
+            g->stage_p = need_p ? (need_t ? set : 0) : -1;
+            g->stage_img = set * ((need_t ? 1 : 0) + (need_p ? 1 : 0));
+        }
         g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
         for (size_t i = 0; i < g->sp.passes.size(); ++i) {
             int S2 = std::min(256, pass_rows(g->sp.passes[i], program(g->sp.passes[i], g->pairs).max_slots, H, acc_sz,
@@ -463,6 +482,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
+        if (g->nby > 0) p->stage_bytes_img = std::max(p->stage_bytes_img, static_cast<size_t>(g->stage_img));
         max_nq = std::max(max_nq, g->qs.n);
         p->additions += g->sp.additions * static_cast<uint64_t>(g->qs.n) * static_cast<uint64_t>(batch);
         p->groups.push_back(std::move(g));
@@ -473,13 +493,16 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     if (const char* e = std::getenv("FHT_CHUNK_IMAGES")) chunk = std::max(1, std::min(batch, std::atoi(e)));
     chunk = std::min(chunk, 65535 / std::max(1, max_nq));
     const size_t cap = size_t(16) << 30;
-    if (max_slot_bytes > 0) chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(chunk, cap / max_slot_bytes)));
+    const size_t per_img = max_slot_bytes + p->stage_bytes_img;
+    if (per_img > 0) chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(chunk, cap / per_img)));
     p->chunk = chunk;
-    p->ws_bytes = max_slot_bytes * static_cast<size_t>(chunk);
+    p->slot_bytes_img = max_slot_bytes;
+    p->ws_bytes = per_img * static_cast<size_t>(chunk);
     const int nchunks = (batch + chunk - 1) / chunk;
     int per_chunk = 0;
     for (auto& g : p->groups)
-        per_chunk += (g->nblocks > 0 ? 1 : 0) + (g->nby > 0 ? 1 : 0) + static_cast<int>(g->sp.passes.size());
+        per_chunk += (g->nblocks > 0 ? 1 : 0) + (g->nby > 0 ? 1 + (g->stage_img > 0 ? 1 : 0) : 0) +
+                     static_cast<int>(g->sp.passes.size());
     p->launches = per_chunk * nchunks;
     return p.release();
 }
@@ -537,6 +560,14 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.passes = g.dt.passes.data();
             L.ws = ws;
             L.nbuf = g.nbuf;
+            // staging after this chunk's slot buffers (execute_host parts hand
+            // each call a workspace sized for its own images)
+            L.stage = g.stage_img > 0 ? static_cast<unsigned char*>(ws) + p->slot_bytes_img * static_cast<size_t>(nimg)
+                                      : nullptr;
+            L.stage_pitch = g.stage_pitch;
+            L.stage_img = g.stage_img;
+            L.stage_t = g.stage_t;
+            L.stage_p = g.stage_p;
             for (int q = 0; q < 4; ++q) L.out.ptr[q] = d_out[q];
             L.out.img_stride = out_stride;
             L.out.layout = p->layout;
@@ -717,7 +748,8 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
             o << (i ? "," : "") << "{\"quadrants\":[";
             for (int k = 0; k < g.qs.n; ++k) o << (k ? "," : "") << g.qs.code[k];
             o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"nbuf\":" << g.nbuf
-              << ",\"pass_rows\":[";
+              << ",\"level_pairs\":" << (g.pairs ? "true" : "false") << ",\"stage_pitch\":" << g.stage_pitch
+              << ",\"stage_bytes\":" << g.stage_img << ",\"pass_rows\":[";
             for (size_t k = 0; k < g.dt.passes.size(); ++k)
                 o << (k ? "," : "") << "[" << g.dt.passes[k].S << "," << g.dt.passes[k].L << "]";
             o << "],\"plan\":" << g.sp.describe() << "}";
@@ -782,8 +814,11 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
                     const int wdt = g.sp.shapes[static_cast<size_t>(b.shape)].width;
                     (g.use_by32 && !g.sp.root_is_block && wdt == 32 ? by_cols : gen_cols) += wdt;
                 }
-                // launch order of launch_group: generic K1, then K1P
+                // launch order of launch_group: generic K1, the u8 staging
+                // (image read + staged columns written), then K1P
                 if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : ea)));
+                if (g.nby > 0 && g.stage_img > 0)
+                    bytes.push_back(nimg * (static_cast<double>(plan->w) * plan->h + static_cast<double>(g.stage_img)));
                 if (g.nby > 0) bytes.push_back(slots * by_cols * H * (ein + ea));
                 for (size_t k = 0; k < g.sp.passes.size(); ++k)
                     bytes.push_back(slots * g.sp.W * H * (ea + (k + 1 == g.sp.passes.size() ? eo : ea)));

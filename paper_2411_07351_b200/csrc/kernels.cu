@@ -460,6 +460,65 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     }
 }
 
+// --------------------------------------------------------------- staging
+// u8 images -> 16-byte aligned working columns for K1P (one aligned 4-byte
+// load per 4 leaves, no wrap arithmetic: rows [H, pitch) repeat rows from 0).
+// One pass over 64 x 64 tiles of the (wrapped) image writes both sets:
+//   T (horizontal quadrants, quadrants.cpp:34-35): T[x][y] = img[y mod h][x],
+//     x < w, y < pitch_t (the tile transposed through shared memory);
+//   P (vertical quadrants, quadrants.cpp:36-37): P[r][y] = img[r][y mod w],
+//     r < h, y < pitch_p.
+// grid: x = 64-column tiles of max(w, pitch_p), y = 64-row tiles of
+// max(h, pitch_t), z = image.  16 byte loads in flight per thread.
+__global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restrict__ img, int w, int h, long long pitch,
+                                                  long long img_stride, int img0, unsigned char* __restrict__ st,
+                                                  long long simg, long long pitch_t, long long off_t, long long pitch_p,
+                                                  long long off_p) {
+    __shared__ __align__(16) unsigned char tile[64][68];
+    const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64, im = blockIdx.z;
+    const bool want_t = off_t >= 0 && c0 < w && r0 < pitch_t;
+    const bool want_p = off_p >= 0 && r0 < h && c0 < pitch_p;
+    if (!want_t && !want_p) return;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+    int c = c0 + tx;
+    if (c >= w) c = c - w < w ? c - w : c % w;
+    const unsigned char* __restrict__ src = img + (size_t)(img0 + im) * img_stride + c;
+    unsigned char v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        int r = r0 + ty + 4 * k;
+        if (r >= h) r = r - h < h ? r - h : r % h;
+        v[k] = src[(size_t)r * pitch];
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[ty + 4 * k][tx] = v[k];
+    __syncthreads();
+    unsigned char* __restrict__ dst = st + (size_t)im * simg;
+    const int j = threadIdx.x & 15;  // 16 words of 4
+    if (want_t) {  // word j of T row x = c0 + cc: rows r0 + 4j .. + 3
+        const long long y = r0 + 4 * j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int cc = (threadIdx.x >> 4) + 16 * k, x = c0 + cc;
+            if (x < w && y < pitch_t) {
+                const uint32_t word = tile[4 * j][cc] | (tile[4 * j + 1][cc] << 8) | (tile[4 * j + 2][cc] << 16) |
+                                      (static_cast<uint32_t>(tile[4 * j + 3][cc]) << 24);
+                *reinterpret_cast<uint32_t*>(dst + off_t + (size_t)x * pitch_t + y) = word;
+            }
+        }
+    }
+    if (want_p) {  // word j of P row r = r0 + rr: columns c0 + 4j .. + 3
+        const long long y = c0 + 4 * j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int rr = (threadIdx.x >> 4) + 16 * k, r = r0 + rr;
+            if (r < h && y < pitch_p)
+                *reinterpret_cast<uint32_t*>(dst + off_p + (size_t)r * pitch_p + y) =
+                    *reinterpret_cast<const uint32_t*>(&tile[rr][4 * j]);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K1P
 // Specialised pass 0 for the common block: a width-32 Brady-Yong subtree
 // (every power-of-two block; all but at most one block of a Tweaked tree).
@@ -606,7 +665,9 @@ template <class In, class Acc, int V>
 __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
                                                           long long img_pitch, long long img_stride, int img0, QuadSet qs, int W, int H,
                                                           int ld, int S, const int* __restrict__ bx0,
-                                                          Acc* __restrict__ ws, int nbuf) {
+                                                          Acc* __restrict__ ws, int nbuf,
+                                                          const unsigned char* __restrict__ stage, long long spitch,
+                                                          long long simg, long long st_t, long long st_p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -620,7 +681,32 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     const int R = S + kBYW - 1;
     Acc* leaves = sm + kBYW * kBYSR;  // parity 1
     constexpr int kRowsPerLane = (kBYMaxS + kBYW - 1 + 31) / 32;  // 9
-    if (q < 2) {
+    if (stage != nullptr) {
+        // staged u8 columns (k_stage_t/p): 4 leaves per aligned 4-byte load,
+        // one 16-byte shared store (lanes contiguous: conflict-free)
+        const unsigned char* __restrict__ sb =
+            stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
+        const int nw = (R + 3) >> 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = warp + h * kWarpsBY;
+            const int col = (q & 1) ? W - 1 - (x0 + c) : x0 + c;
+            const uint32_t* __restrict__ cp = reinterpret_cast<const uint32_t*>(sb + (size_t)col * spitch);
+            uint32_t v[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (lane + 32 * k < nw) v[k] = __ldg(cp + lane + 32 * k);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (lane + 32 * k < nw) {
+                    const uint32_t x = v[k];
+                    sts4(leaves + c * kBYSR + 4 * (lane + 32 * k),
+                         make_int4(to_bits<Acc>(static_cast<Acc>(x & 0xff)), to_bits<Acc>(static_cast<Acc>((x >> 8) & 0xff)),
+                                   to_bits<Acc>(static_cast<Acc>((x >> 16) & 0xff)),
+                                   to_bits<Acc>(static_cast<Acc>(x >> 24))));
+                }
+        }
+    } else if (q < 2) {
         // image rows: 32 contiguous pixels per tile row; stage row-major
         // (stride 33, conflict-free both ways) in parity 0, then transpose.
         Acc* stage = sm;
@@ -1034,6 +1120,18 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         if (hook) hook(ctx, 1);
     }
     if constexpr (sizeof(Acc) == 4) {
+        const unsigned char* stage = nullptr;
+        if (g.nby > 0 && g.stage != nullptr && std::is_same<In, unsigned char>::value) {
+            const auto* im = reinterpret_cast<const unsigned char*>(g.img);
+            const long long ext_w = std::max<long long>(g.img_w, g.stage_p >= 0 ? g.stage_pitch : 0);
+            const long long ext_h = std::max<long long>(g.img_h, g.stage_t >= 0 ? g.stage_pitch : 0);
+            dim3 gs(static_cast<unsigned>((ext_w + 63) / 64), static_cast<unsigned>((ext_h + 63) / 64), g.nimg);
+            k_stage_u8<<<gs, 256, 0, st>>>(im, g.img_w, g.img_h, g.img_pitch, g.img_stride, g.img0, g.stage, g.stage_img,
+                                           g.stage_pitch, g.stage_t, g.stage_pitch, g.stage_p);
+            ++launches;
+            if (hook) hook(ctx, 5);
+            stage = g.stage;
+        }
         if (g.nby > 0) {
             auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
                       : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>
@@ -1042,7 +1140,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
             kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                              g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf);
+                                              g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf,
+                                              stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
             ++launches;
             if (hook) hook(ctx, 4);
         }

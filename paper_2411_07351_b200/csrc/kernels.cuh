@@ -96,6 +96,13 @@ struct GroupLaunch {
     void* ws;
     int nbuf;
     OutDesc out;
+    // u8 staging for K1P (null: K1P reads the image itself): per image, the
+    // working columns of the horizontal quadrants (image columns, at
+    // stage_t) and/or of the vertical ones (image rows, at stage_p), W
+    // columns of stage_pitch bytes each, rows past H wrapped
+    unsigned char* stage;
+    long long stage_pitch, stage_img;
+    long long stage_t, stage_p;  // byte offsets inside an image's stage (-1: not staged)
 };
 
 size_t k1_smem_bytes(int acc_dtype, int max_width, int sr, int max_ops, int max_steps);

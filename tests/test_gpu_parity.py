@@ -126,9 +126,9 @@ def test_float32_small_bit_exact_vs_fp32_tree():
             np.testing.assert_array_equal(out[k][0], ref[k])
 
 
-@pytest.mark.parametrize("k1p,k2,pairs,bulk", [(0, 0, 0, 0), (2, 0, 0, 0), (2, 1, 0, 0), (3, 0, 0, 1), (3, 1, 0, 0),
-                                              (3, 1, 1, 0), (3, 1, 1, 1)])
-def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk):
+@pytest.mark.parametrize("k1p,k2,pairs,bulk,stage", [(0, 0, 0, 0, 0), (2, 0, 0, 0, 1), (2, 1, 0, 0, 0), (3, 0, 0, 1, 1),
+                                                    (3, 1, 0, 0, 0), (3, 1, 1, 0, 1), (3, 1, 1, 1, 0), (0, 1, 1, 0, 1)])
+def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk, stage):
     """Every K1P level variant (0: all levels in shared memory, 2: levels 1-2
     in registers, 3: + interleaved levels 3-5), both one-level K2 merge
     layouts (0: 4 rows per lane, 1: rows interleaved over lanes), the
@@ -138,6 +138,7 @@ def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk):
     monkeypatch.setenv("FHT_K2_SCALAR", str(k2))
     monkeypatch.setenv("FHT_K2_PAIRS", str(pairs))
     monkeypatch.setenv("FHT_K2_BULK", str(bulk))
+    monkeypatch.setenv("FHT_K1_STAGE", str(stage))  # u8 images staged as aligned columns for K1P
     rng = np.random.default_rng(40 + 10 * k1p + k2)
     for strategy, (h, w) in [(1, (509, 509)), (0, (300, 257)), (1, (1000, 70))]:
         imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)
@@ -252,7 +253,7 @@ def test_execute_host_roundtrip():
             np.testing.assert_array_equal(out[k][bi], ref[k])
 
 
-def test_profiled_launch_accounting():
+def test_profiled_launch_accounting(monkeypatch):
     """fht_execute_profiled: one record per launch, kinds in launch order and
     algorithmic bytes that add up to the plan's passes (bench roofline input)."""
     import ctypes
@@ -260,6 +261,7 @@ def test_profiled_launch_accounting():
     from paper_2411_07351_b200._lib import check, lib
 
     n = 509
+    monkeypatch.setenv("FHT_K1_STAGE", "1")  # staged even for this small batch
     plan = fht.Plan(n, n, "tweaked", in_dtype="u8", acc_dtype="i32", batch=3)
     x = torch.zeros((3, n, n), dtype=torch.uint8, device="cuda")
     out = plan.alloc_outputs()
@@ -269,10 +271,15 @@ def test_profiled_launch_accounting():
     ms, kind, by, got = (ctypes.c_float * nl)(), (ctypes.c_int * nl)(), (ctypes.c_double * nl)(), ctypes.c_int()
     check(lib().fht_execute_profiled(plan._h, ctypes.c_void_p(x.data_ptr()), n * n, ptrs, n * n,
                                      ctypes.c_void_p(ws.data_ptr()), None, ms, kind, by, nl, ctypes.byref(got)))
-    assert got.value == nl == 3
+    assert got.value == nl == 4
     kinds, b = list(kind), list(by)
-    assert kinds == [1, 4, 3]  # generic K1 (remainder block), K1P, root band
+    # generic K1 (remainder block), u8 staging of the horizontal (T) and
+    # vertical (P) working columns, K1P, root band
+    assert kinds == [1, 5, 4, 3]
     slots, cells = 3 * 4, n * n
-    assert b[0] + b[1] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
-    assert b[1] == slots * (n // 32) * 32 * n * 5  # the 15 width-32 blocks
-    assert b[2] == slots * cells * 8
+    assert b[0] + b[2] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
+    assert b[2] == slots * (n // 32) * 32 * n * 5  # the 15 width-32 blocks
+    assert b[3] == slots * cells * 8
+    pitch = plan.describe()["groups"][0]["stage_pitch"]
+    assert pitch % 16 == 0 and pitch >= n + 31
+    assert b[1] == 3 * (cells + 2 * n * pitch)  # image read + both staged column sets written
