@@ -814,11 +814,11 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
                     const int wdt = g.sp.shapes[static_cast<size_t>(b.shape)].width;
                     (g.use_by32 && !g.sp.root_is_block && wdt == 32 ? by_cols : gen_cols) += wdt;
                 }
-                // launch order of launch_group: generic K1, the u8 staging
-                // (image read + staged columns written), then K1P
-                if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : ea)));
+                // launch order of launch_group: the u8 staging (image read +
+                // staged columns written), generic K1, then K1P
                 if (g.nby > 0 && g.stage_img > 0)
                     bytes.push_back(nimg * (static_cast<double>(plan->w) * plan->h + static_cast<double>(g.stage_img)));
+                if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : ea)));
                 if (g.nby > 0) bytes.push_back(slots * by_cols * H * (ein + ea));
                 for (size_t k = 0; k < g.sp.passes.size(); ++k)
                     bytes.push_back(slots * g.sp.W * H * (ea + (k + 1 == g.sp.passes.size() ? eo : ea)));

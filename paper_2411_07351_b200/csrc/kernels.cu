@@ -356,14 +356,15 @@ __device__ __forceinline__ void warp_store_col(Out* __restrict__ g, const Acc* s
 
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
-template <class In, class Acc, class Out>
+template <class In, class Acc, class Out, bool SC>
 __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const In* __restrict__ img, int img_w, int img_h, long long img_pitch, long long img_stride, int img0, QuadSet qs,
     int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
     const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, const int4* __restrict__ bops, int max_width,
     int sr, int max_ops,
-    Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out) {
+    Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
+    long long spitch, long long simg, long long st_t, long long st_p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
     Acc* buf1 = buf0 + (size_t)max_width * sr;     // slots [max_width, 2 max_width): parity 1
@@ -386,7 +387,22 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     Acc* lbuf = (nsteps & 1) ? buf1 : buf0;
     const int warp = tid >> 5, lane = tid & 31;
     constexpr int kWarps = kThreads / 32;
-    if (q < 2) {
+    if (stage != nullptr) {
+        // staged u8 columns (k_stage_u8): 4 leaves per aligned 4-byte load
+        const unsigned char* __restrict__ sb =
+            stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
+        const int nw = (R + 3) >> 2;
+        for (int c = warp; c < wb; c += kWarps) {
+            const int col = (q & 1) ? W - 1 - (x0 + c) : x0 + c;
+            const uint32_t* __restrict__ cp = reinterpret_cast<const uint32_t*>(sb + (size_t)col * spitch);
+            for (int k = lane; k < nw; k += 32) {
+                const uint32_t x = __ldg(cp + k);
+                sts4(lbuf + c * sr + 4 * k,
+                     make_int4(to_bits<Acc>(static_cast<Acc>(x & 0xff)), to_bits<Acc>(static_cast<Acc>((x >> 8) & 0xff)),
+                               to_bits<Acc>(static_cast<Acc>((x >> 16) & 0xff)), to_bits<Acc>(static_cast<Acc>(x >> 24))));
+            }
+        }
+    } else if (q < 2) {
         // working column = image column (flipped for horiz_neg): a tile row is
         // wb contiguous image pixels.  Stage row-major (row stride wb+1, so
         // both the row writes and the column reads below are bank-conflict
@@ -433,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     for (int k = 0; k < nsteps; ++k) {
         __syncthreads();
         if constexpr (sizeof(Acc) == 4)
-            run_step_baked<Acc, kWarps>(smem_u32(buf0), bops + hdr.op_base, step_offs[hdr.step_base + k],
-                                        step_offs[hdr.step_base + k + 1], warp, lane);
+            run_step_baked<Acc, kWarps, SC>(smem_u32(buf0), bops + hdr.op_base, step_offs[hdr.step_base + k],
+                                            step_offs[hdr.step_base + k + 1], warp, lane);
         else
             run_step<Acc, kWarps>(buf0, sr, ops + hdr.op_base, step_offs[hdr.step_base + k],
                                   step_offs[hdr.step_base + k + 1], S, warp, lane);
@@ -1098,30 +1114,15 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     int launches = 0;
     const int nslots = g.nimg * g.qs.n;
     const size_t smem = k1_smem_bytes(g.acc_dtype, g.k1_max_width, g.k1_sr, g.k1_max_ops, g.k1_max_steps);
-    auto k1 = k1_blocks<In, Acc, Out>;
-    allow_smem(reinterpret_cast<const void*>(k1));
     Acc* ws = reinterpret_cast<Acc*>(g.ws);
     // Pass 0: the width-32 Brady-Yong blocks (K1P) and the other blocks (K1)
     // write disjoint columns; when both exist, K1 runs concurrently on the
-    // plan's auxiliary stream (joined by an event before the first K2 pass).
-    const bool both = (sizeof(Acc) == 4) && g.nby > 0 && g.nblocks > 0 && g.aux_stream && !hook;
-    cudaStream_t st1 = both ? g.aux_stream : st;
-    if (both) {
-        cudaEventRecord(g.ev_fork, st);
-        cudaStreamWaitEvent(st1, g.ev_fork, 0);
-    }
-    if (g.nblocks > 0) {
-        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
-        k1<<<g1, kThreads, smem, st1>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                        g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes,
-                                        g.step_offs, g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws,
-                                        g.nbuf, g.root_is_block, g.out);
-        ++launches;
-        if (hook) hook(ctx, 1);
-    }
-    if constexpr (sizeof(Acc) == 4) {
-        const unsigned char* stage = nullptr;
-        if (g.nby > 0 && g.stage != nullptr && std::is_same<In, unsigned char>::value) {
+    // plan's auxiliary stream (forked after the staging, joined by an event
+    // before the first K2 pass).
+    // u8 staging (large batches): the aligned working columns K1 and K1P read
+    const unsigned char* stage = nullptr;
+    if constexpr (sizeof(Acc) == 4 && std::is_same<In, unsigned char>::value) {
+        if (g.nby > 0 && g.stage != nullptr) {
             const auto* im = reinterpret_cast<const unsigned char*>(g.img);
             const long long ext_w = std::max<long long>(g.img_w, g.stage_p >= 0 ? g.stage_pitch : 0);
             const long long ext_h = std::max<long long>(g.img_h, g.stage_t >= 0 ? g.stage_pitch : 0);
@@ -1132,6 +1133,26 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             if (hook) hook(ctx, 5);
             stage = g.stage;
         }
+    }
+    const bool both = (sizeof(Acc) == 4) && g.nby > 0 && g.nblocks > 0 && g.aux_stream && !hook;
+    cudaStream_t st1 = both ? g.aux_stream : st;
+    if (both) {
+        cudaEventRecord(g.ev_fork, st);
+        cudaStreamWaitEvent(st1, g.ev_fork, 0);
+    }
+    if (g.nblocks > 0) {
+        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
+        auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;
+        allow_smem(reinterpret_cast<const void*>(k1));
+        k1<<<g1, kThreads, smem, st1>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
+                                        g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes,
+                                        g.step_offs, g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws,
+                                        g.nbuf, g.root_is_block, g.out, stage, g.stage_pitch, g.stage_img, g.stage_t,
+                                        g.stage_p);
+        ++launches;
+        if (hook) hook(ctx, 1);
+    }
+    if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
             auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
                       : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>

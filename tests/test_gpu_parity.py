@@ -273,13 +273,13 @@ def test_profiled_launch_accounting(monkeypatch):
                                      ctypes.c_void_p(ws.data_ptr()), None, ms, kind, by, nl, ctypes.byref(got)))
     assert got.value == nl == 4
     kinds, b = list(kind), list(by)
-    # generic K1 (remainder block), u8 staging of the horizontal (T) and
-    # vertical (P) working columns, K1P, root band
-    assert kinds == [1, 5, 4, 3]
+    # u8 staging of the horizontal (T) and vertical (P) working columns,
+    # generic K1 (remainder block), K1P, root band
+    assert kinds == [5, 1, 4, 3]
     slots, cells = 3 * 4, n * n
-    assert b[0] + b[2] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
+    assert b[1] + b[2] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
     assert b[2] == slots * (n // 32) * 32 * n * 5  # the 15 width-32 blocks
     assert b[3] == slots * cells * 8
     pitch = plan.describe()["groups"][0]["stage_pitch"]
     assert pitch % 16 == 0 and pitch >= n + 31
-    assert b[1] == 3 * (cells + 2 * n * pitch)  # image read + both staged column sets written
+    assert b[0] == 3 * (cells + 2 * n * pitch)  # image read + both staged column sets written
