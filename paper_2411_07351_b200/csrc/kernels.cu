@@ -604,6 +604,37 @@ __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
     }
 }
 
+// Level 5 (the block root) written straight to the pass-0 buffer from
+// registers: lane = row, so each warp store is 32 consecutive rows of one
+// column (coalesced), and the root never round-trips through shared memory.
+template <class Acc>
+__device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+                                                int rows_out) {
+    constexpr int w = 32, w0 = 16;
+    constexpr int src = 0;  // level 4 output (parity of V3): slots [0, 32)
+    constexpr int G = (kBYMaxS + 31) / 32;
+    const uint32_t base = smem_u32(sm) + lane * 4u;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        const int T = warp + h * kWarpsBY;
+        const int t0 = (2 * T * (w0 - 1) + (w - 1)) / (2 * (w - 1));
+        const int r = T - t0;
+        const uint32_t a = base + (src + t0) * kBYSR * 4u;
+        const uint32_t b = base + ((src + w0 + t0) * kBYSR + r) * 4u;
+        Acc* __restrict__ g = dcol0 + (size_t)T * ld + lane;
+        int x[G], y[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            if (32 * u + lane < rows_out) {
+                x[u] = lds1u(a + 128u * u);
+                y[u] = lds1u(b + 128u * u);
+            }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            if (32 * u + lane < rows_out) g[32 * u] = from_bits<Acc>(add_bits<Acc>(x[u], y[u]));
+    }
+}
+
 template <class Acc, int L, int F = 0>
 __device__ __forceinline__ void by_level_v0(Acc* sm, int S, int warp, int lane) {
     constexpr int w = 1 << L, w0 = w >> 1;
@@ -774,7 +805,17 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         }
     }
     __syncthreads();
-    if constexpr (V == 3) {
+    if constexpr (V == 4) {
+        by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
+        __syncthreads();
+        by_level_s<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 4>(sm, S, warp, lane);  // -> slots [0, 32)
+        __syncthreads();
+        by_level5_store<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+                             min(S, H - s0));
+        return;
+    } else if constexpr (V == 3) {
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
         by_level_s<Acc, 3>(sm, S, warp, lane);
@@ -1156,7 +1197,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         if (g.nby > 0) {
             auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
                       : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>
-                                           : k1_by32<In, Acc, 3>;
+                      : g.k1p_variant == 3 ? k1_by32<In, Acc, 3>
+                                           : k1_by32<In, Acc, 4>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
