@@ -412,7 +412,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             for (const auto& ps : g->sp.passes) {
                 const PassProgram pr = program(ps, g->pairs);
                 const int rows = pass_rows(ps, pr.max_slots, H, acc_sz, budget);
-                const int Lmax = std::min(rows, 256) + ps.max_ext + 20;
+                const int Lmax = std::min(rows, env_int("FHT_K2_SMAX", 256, 32, 4096)) + ps.max_ext + 20;
                 ok = ok && rows >= std::min(H, 32) &&
                      fhtb::k2_smem_bytes(acc, pr.max_slots, Lmax, pr.max_tile_ops()) <= 227 * 1024;
             }
@@ -459,8 +459,8 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         }
         g->slot_bytes = static_cast<size_t>(g->nbuf) * W * g->ld * acc_sz;
         for (size_t i = 0; i < g->sp.passes.size(); ++i) {
-            int S2 = std::min(256, pass_rows(g->sp.passes[i], program(g->sp.passes[i], g->pairs).max_slots, H, acc_sz,
-                                             budget));
+            int S2 = std::min(env_int("FHT_K2_SMAX", 256, 32, 4096),
+                              pass_rows(g->sp.passes[i], program(g->sp.passes[i], g->pairs).max_slots, H, acc_sz, budget));
             {  // balance the row tiles
                 const int nt = (H + S2 - 1) / std::max(1, S2);
                 S2 = std::min(S2, ((H + nt - 1) / nt + 7) & ~7);

@@ -1046,21 +1046,35 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
             const int sl0 = lane < nc ? ps.stores[tile.store_beg + lane].x : 0;
             const int sl1 = lane + 32 < nc ? ps.stores[tile.store_beg + lane + 32].x : 0;
             if constexpr (sizeof(Acc) == 4) {
-                // lane = slope; 16-byte smem reads of 4 rows, 4 coalesced row stores
-                for (int i = warp * 4; i < rows; i += kWarps * 4) {
-                    Out* __restrict__ orow = o + (size_t)(s0 + i) * W + t0;
-                    const int nr = min(4, rows - i);
+                // lane = slope; 16-byte smem reads of 4 rows, 4 coalesced row
+                // stores; one row pointer per warp advanced by a fixed stride
+                // (the 64-bit address math per store dominated otherwise)
+                const uint32_t sa0 = smem_u32(sm + (size_t)sl0 * L), sa1 = smem_u32(sm + (size_t)sl1 * L);
+                const size_t wstep = (size_t)W * (kWarps * 4);
+                Out* __restrict__ prow = o + (size_t)(s0 + warp * 4) * W + t0 + lane;
+                int i = warp * 4;
+                for (; i + 4 <= rows; i += kWarps * 4, prow += wstep) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int c = lane + 32 * h;
-                        if (c >= nc) continue;
-                        // one 16-byte read (the compiler splits a C++ int4 load
-                        // it cannot prove aligned into two conflicting LDS.64)
-                        const int4 v4 = lds4u(smem_u32(sm + (size_t)(h ? sl1 : sl0) * L + i));
+                        if (lane + 32 * h >= nc) continue;
+                        const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
+                        Out* __restrict__ p = prow + 32 * h;
+                        p[0] = static_cast<Out>(from_bits<Acc>(v4.x));
+                        p[W] = static_cast<Out>(from_bits<Acc>(v4.y));
+                        p[2 * W] = static_cast<Out>(from_bits<Acc>(v4.z));
+                        p[3 * W] = static_cast<Out>(from_bits<Acc>(v4.w));
+                    }
+                }
+                if (i < rows) {  // the last 1-3 rows
+                    const int nr = rows - i;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (lane + 32 * h >= nc) continue;
+                        const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
                         const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            if (k < nr) orow[(size_t)k * W + c] = static_cast<Out>(from_bits<Acc>(vv[k]));
+                            if (k < nr) prow[32 * h + (size_t)k * W] = static_cast<Out>(from_bits<Acc>(vv[k]));
                     }
                 }
             } else {
