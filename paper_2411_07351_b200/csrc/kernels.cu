@@ -707,6 +707,48 @@ __device__ __forceinline__ void by_level12(Acc* sm, int S, int tid) {
     }
 }
 
+// Levels 1-2 straight from the staged u8 columns (k_stage_u8): the same
+// items as by_level12, the leaf vectors unpacked from aligned 4-byte global
+// loads (lanes over consecutive row chunks: coalesced) instead of a leaf
+// tile in shared memory -- the leaves never touch shared memory.
+template <class Acc>
+__device__ __forceinline__ int4 unpack_u8x4(uint32_t x) {
+    return make_int4(to_bits<Acc>(static_cast<Acc>(x & 0xff)), to_bits<Acc>(static_cast<Acc>((x >> 8) & 0xff)),
+                     to_bits<Acc>(static_cast<Acc>((x >> 16) & 0xff)), to_bits<Acc>(static_cast<Acc>(x >> 24)));
+}
+template <class Acc>
+__device__ __forceinline__ void by_level12_staged(Acc* sm, int S, int tid, const unsigned char* __restrict__ sb,
+                                                  long long spitch, int W, int x0, bool rev) {
+    const int nchunk = (S + kBYW - 4 + 3) >> 2;
+    const int items = 8 * nchunk;
+    int4* O = reinterpret_cast<int4*>(sm);
+    constexpr int s4 = kBYSR / 4;
+    for (int it = tid; it < items; it += kThreadsBY) {
+        const int g = it / nchunk, j = it - g * nchunk;
+        const int c = x0 + 4 * g;
+        const long long cs = rev ? -spitch : spitch;  // reversed column order for horiz_neg / vert_neg
+        const unsigned char* pa = sb + (long long)(rev ? W - 1 - c : c) * spitch + 4 * j;
+        const uint32_t* A = reinterpret_cast<const uint32_t*>(pa);
+        const uint32_t* B = reinterpret_cast<const uint32_t*>(pa + cs);
+        const uint32_t* E = reinterpret_cast<const uint32_t*>(pa + 2 * cs);
+        const uint32_t* F = reinterpret_cast<const uint32_t*>(pa + 3 * cs);
+        const uint32_t wa0 = __ldg(A), wb0 = __ldg(B), wb1 = __ldg(B + 1), we0 = __ldg(E), we1 = __ldg(E + 1),
+                       wf0 = __ldg(F), wf1 = __ldg(F + 1);
+        const int4 a0 = unpack_u8x4<Acc>(wa0), b0 = unpack_u8x4<Acc>(wb0), b1 = unpack_u8x4<Acc>(wb1);
+        const int4 e0 = unpack_u8x4<Acc>(we0), e1 = unpack_u8x4<Acc>(we1), f0 = unpack_u8x4<Acc>(wf0),
+                   f1 = unpack_u8x4<Acc>(wf1);
+        const int4 p0l = add4<Acc>(a0, b0);
+        const int4 p1l = add4<Acc>(a0, shifted<1>(b0, b1));
+        const int4 q0l = add4<Acc>(e0, f0), q0h = add4<Acc>(e1, f1);
+        const int4 q1l = add4<Acc>(e0, shifted<1>(f0, f1)), q1h = add4<Acc>(e1, shifted<1>(f1, f1));
+        const int d0 = (4 * g) * s4 + j;
+        O[d0] = add4<Acc>(p0l, q0l);
+        O[d0 + s4] = add4<Acc>(p0l, shifted<1>(q0l, q0h));
+        O[d0 + 2 * s4] = add4<Acc>(p1l, shifted<1>(q1l, q1h));
+        O[d0 + 3 * s4] = add4<Acc>(p1l, shifted<2>(q1l, q1h));
+    }
+}
+
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
 template <class In, class Acc, int V>
 __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
@@ -728,6 +770,20 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     const int R = S + kBYW - 1;
     Acc* leaves = sm + kBYW * kBYSR;  // parity 1
     constexpr int kRowsPerLane = (kBYMaxS + kBYW - 1 + 31) / 32;  // 9
+    if (V == 5 && stage != nullptr) {
+        // levels 1-2 read the staged columns directly (no leaf tile)
+        const unsigned char* __restrict__ sb =
+            stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
+        by_level12_staged<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
+        __syncthreads();
+        by_level_s<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 4>(sm, S, warp, lane);  // -> slots [0, 32)
+        __syncthreads();
+        by_level5_store<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+                             min(S, H - s0));
+        return;
+    }
     if (stage != nullptr) {
         // staged u8 columns (k_stage_t/p): 4 leaves per aligned 4-byte load,
         // one 16-byte shared store (lanes contiguous: conflict-free)
@@ -805,7 +861,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         }
     }
     __syncthreads();
-    if constexpr (V == 4) {
+    if constexpr (V >= 4) {  // (V = 5 without staging lands here)
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
         by_level_s<Acc, 3>(sm, S, warp, lane);
@@ -1212,7 +1268,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
                       : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>
                       : g.k1p_variant == 3 ? k1_by32<In, Acc, 3>
-                                           : k1_by32<In, Acc, 4>;
+                      : g.k1p_variant == 4 ? k1_by32<In, Acc, 4>
+                                           : k1_by32<In, Acc, 5>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);

@@ -79,9 +79,11 @@ struct GroupLaunch {
     const int* by_x0;
     cudaStream_t aux_stream;  // plan-owned stream for the concurrent generic-block K1 (may be null)
     cudaEvent_t ev_fork, ev_join;
-    int k1p_variant;    // 4 (default): levels 1-2 in registers, 3-5 rows interleaved over lanes, the
-                        // root stored from registers; 3: root via shared memory; 2: levels 3-5
-                        // with 4 rows per lane; 0: all levels in shared memory
+    int k1p_variant;    // 5 (default): 4, with levels 1-2 reading the staged u8 columns directly
+                        // (no leaf tile) when the input is staged; 4: levels 1-2 in registers,
+                        // 3-5 rows interleaved over lanes, the root stored from registers;
+                        // 3: root via shared memory; 2: levels 3-5 with 4 rows per lane;
+                        // 0: all levels in shared memory
     int k2_bulk;        // K2 aligned window runs by cp.async.bulk (TMA) instead of 16-byte cp.async
     int k2_scalar;      // 1 (default): K2 merge rows interleaved over lanes; 0: 4 rows per lane (int4)
     const ShapeHdr* shapes;

@@ -127,7 +127,7 @@ def test_float32_small_bit_exact_vs_fp32_tree():
 
 
 @pytest.mark.parametrize("k1p,k2,pairs,bulk,stage", [(0, 0, 0, 0, 0), (2, 0, 0, 0, 1), (2, 1, 0, 0, 0), (3, 0, 0, 1, 1), (4, 1, 1, 0, 1), (4, 0, 0, 0, 0),
-                                                    (3, 1, 0, 0, 0), (3, 1, 1, 0, 1), (3, 1, 1, 1, 0), (0, 1, 1, 0, 1)])
+                                                    (3, 1, 0, 0, 0), (3, 1, 1, 0, 1), (3, 1, 1, 1, 0), (0, 1, 1, 0, 1), (5, 1, 1, 0, 1), (5, 1, 1, 0, 0)])
 def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk, stage):
     """Every K1P level variant (0: all levels in shared memory, 2: levels 1-2
     in registers, 3: + interleaved levels 3-5), both one-level K2 merge
