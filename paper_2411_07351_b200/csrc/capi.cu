@@ -544,6 +544,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.k1p_variant = env_int("FHT_K1P_VARIANT", 5, 0, 5);  // see GroupLaunch
             L.k2_scalar = env_int("FHT_K2_SCALAR", 1, 0, 1);
             L.k2_bulk = env_int("FHT_K2_BULK", 0, 0, 1);
+            L.pdl = env_int("FHT_PDL", 1, 0, 1);
             L.aux_stream = env_int("FHT_K1_OVERLAP", 1, 0, 1) ? p->aux : nullptr;
             L.ev_fork = p->ev_fork;
             L.ev_join = p->ev_join;

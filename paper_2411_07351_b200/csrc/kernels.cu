@@ -354,6 +354,32 @@ __device__ __forceinline__ void warp_store_col(Out* __restrict__ g, const Acc* s
 }
 
 
+// Programmatic dependent launch: the kernel is queued while its stream
+// predecessor drains and waits at griddepcontrol.wait (its first statement)
+// for the predecessor's results; hides the launch gap between the short
+// dependent launches of small transforms.  No early trigger: a dependent
+// never holds shared memory a running predecessor still needs.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    if (!pdl) {
+        kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
 template <class In, class Acc, class Out, bool SC>
@@ -365,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
     long long spitch, long long simg, long long st_t, long long st_p) {
+    grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
     Acc* buf1 = buf0 + (size_t)max_width * sr;     // slots [max_width, 2 max_width): parity 1
@@ -490,6 +517,7 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
                                                   long long img_stride, int img0, unsigned char* __restrict__ st,
                                                   long long simg, long long pitch_t, long long off_t, long long pitch_p,
                                                   long long off_p) {
+    grid_dep_wait();
     __shared__ __align__(16) unsigned char tile[64][68];
     const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64, im = blockIdx.z;
     const bool want_t = off_t >= 0 && c0 < w && r0 < pitch_t;
@@ -757,6 +785,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
                                                           Acc* __restrict__ ws, int nbuf,
                                                           const unsigned char* __restrict__ stage, long long spitch,
                                                           long long simg, long long st_t, long long st_p) {
+    grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1014,6 +1043,7 @@ template <class Acc, class Out, int MODE>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
+    grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1238,8 +1268,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             const long long ext_w = std::max<long long>(g.img_w, g.stage_p >= 0 ? g.stage_pitch : 0);
             const long long ext_h = std::max<long long>(g.img_h, g.stage_t >= 0 ? g.stage_pitch : 0);
             dim3 gs(static_cast<unsigned>((ext_w + 63) / 64), static_cast<unsigned>((ext_h + 63) / 64), g.nimg);
-            k_stage_u8<<<gs, 256, 0, st>>>(im, g.img_w, g.img_h, g.img_pitch, g.img_stride, g.img0, g.stage, g.stage_img,
-                                           g.stage_pitch, g.stage_t, g.stage_pitch, g.stage_p);
+            launch_k(g.pdl, k_stage_u8, gs, dim3(256), 0, st, im, g.img_w, g.img_h, g.img_pitch, g.img_stride, g.img0,
+                     g.stage, g.stage_img, g.stage_pitch, g.stage_t, g.stage_pitch, g.stage_p);
             ++launches;
             if (hook) hook(ctx, 5);
             stage = g.stage;
@@ -1255,11 +1285,10 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
         auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;
         allow_smem(reinterpret_cast<const void*>(k1));
-        k1<<<g1, kThreads, smem, st1>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                        g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes,
-                                        g.step_offs, g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws,
-                                        g.nbuf, g.root_is_block, g.out, stage, g.stage_pitch, g.stage_img, g.stage_t,
-                                        g.stage_p);
+        launch_k(g.pdl && !both, k1, g1, dim3(kThreads), smem, st1, reinterpret_cast<const In*>(g.img), g.img_w,
+                 g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs,
+                 g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out, stage,
+                 g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
         ++launches;
         if (hook) hook(ctx, 1);
     }
@@ -1273,9 +1302,9 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             allow_smem(reinterpret_cast<const void*>(kb));
             dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
-            kb<<<gb, kThreadsBY, sm_by, st>>>(reinterpret_cast<const In*>(g.img), g.img_w, g.img_h, g.img_pitch,
-                                              g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf,
-                                              stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
+            launch_k(g.pdl, kb, gb, dim3(kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w, g.img_h,
+                     g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf, stage,
+                     g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
             ++launches;
             if (hook) hook(ctx, 4);
         }
@@ -1301,7 +1330,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         pd.bulk = g.k2_bulk;
         allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
-        k2<<<g2, kThreads2, smem2, st>>>(pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out, g.qs, g.img0);
+        launch_k(g.pdl, k2, g2, dim3(kThreads2), smem2, st, pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out,
+                 g.qs, g.img0);
         ++launches;
         if (hook) hook(ctx, final_pass ? 3 : 2);
     }

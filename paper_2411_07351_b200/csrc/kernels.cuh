@@ -84,6 +84,7 @@ struct GroupLaunch {
                         // 3-5 rows interleaved over lanes, the root stored from registers;
                         // 3: root via shared memory; 2: levels 3-5 with 4 rows per lane;
                         // 0: all levels in shared memory
+    int pdl;            // programmatic dependent launch of the stream-ordered kernels
     int k2_bulk;        // K2 aligned window runs by cp.async.bulk (TMA) instead of 16-byte cp.async
     int k2_scalar;      // 1 (default): K2 merge rows interleaved over lanes; 0: 4 rows per lane (int4)
     const ShapeHdr* shapes;
