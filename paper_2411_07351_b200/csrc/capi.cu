@@ -403,7 +403,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         // Fused-pass tiles: shrink the tile width until every pass gets a
         // reasonable row tile in the shared-memory budget.
         const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 105, 16, 220)) * 1024;
-        const int levels = env_int("FHT_PASS_LEVELS", 4, 1, 8);
+        const int levels = env_int("FHT_PASS_LEVELS", 5, 1, 8);
         int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
         g->pairs = acc_sz == 4 && env_int("FHT_K2_PAIRS", 1, 0, 1) == 1;
         for (;;) {

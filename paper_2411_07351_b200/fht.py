@@ -108,7 +108,7 @@ def count_additions_tree(w: int, h: int, strategy=SplitStrategy.Tweaked) -> int:
     return int(r.value)
 
 
-def schedule(W: int, H: int, strategy=SplitStrategy.Tweaked, block_width: int = 32, pass_levels: int = 4,
+def schedule(W: int, H: int, strategy=SplitStrategy.Tweaked, block_width: int = 32, pass_levels: int = 5,
              tile_width: int = 32) -> dict:
     """The host schedule tables for one orientation (no GPU needed)."""
     need = ctypes.c_size_t()
