@@ -47,6 +47,22 @@ constexpr int kU = 8;  // independent global loads in flight per lane
 template <class Acc, class Src>
 __device__ __forceinline__ void warp_load_window(Acc* __restrict__ d, const Src* __restrict__ col, int start, int n,
                                                  int H, int lane) {
+    if (start + n <= H) {  // no wrap: plain contiguous run
+        for (int i0 = 0; i0 < n; i0 += 32 * kU) {
+            Src v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < n) v[u] = col[start + i];
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * 32 + lane;
+                if (i < n) d[i] = static_cast<Acc>(v[u]);
+            }
+        }
+        return;
+    }
     for (int i0 = 0; i0 < n; i0 += 32 * kU) {
         Src v[kU];
 #pragma unroll
@@ -446,7 +462,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
             for (int u = 0; u < kUH; ++u) {
                 const int i = ib + u * kWarps;
                 if (i < R) {
-                    const In* __restrict__ rowp = im + (size_t)wrap_any(s0 + i, H) * img_pitch;
+                    const int y = s0 + R <= H ? s0 + i : wrap_any(s0 + i, H);  // tile-uniform test
+                    const In* __restrict__ rowp = im + (size_t)y * img_pitch;
                     if (lane < wb) v[u][0] = rowp[xa + dx * lane];
                     if (lane + 32 < wb) v[u][1] = rowp[xa + dx * (lane + 32)];
                 }
@@ -845,10 +862,18 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         const int xx = (q == 1) ? img_w - 1 - (x0 + lane) : x0 + lane;
         constexpr int kRowsPerWarp = (kBYMaxS + kBYW - 1 + kWarpsBY - 1) / kWarpsBY;  // 18
         In v[kRowsPerWarp];
+        if (s0 + R <= H) {  // no wrap in this row tile (all but the last): one pointer stride
+            const In* __restrict__ p = im + (size_t)(s0 + warp) * img_pitch + xx;
+            const size_t step = (size_t)kWarpsBY * img_pitch;
 #pragma unroll
-        for (int k = 0; k < kRowsPerWarp; ++k) {
-            const int i = warp + k * kWarpsBY;
-            if (i < R) v[k] = im[(size_t)wrap_any(s0 + i, H) * img_pitch + xx];
+            for (int k = 0; k < kRowsPerWarp; ++k)
+                if (warp + k * kWarpsBY < R) v[k] = p[k * step];
+        } else {
+#pragma unroll
+            for (int k = 0; k < kRowsPerWarp; ++k) {
+                const int i = warp + k * kWarpsBY;
+                if (i < R) v[k] = im[(size_t)wrap_any(s0 + i, H) * img_pitch + xx];
+            }
         }
 #pragma unroll
         for (int k = 0; k < kRowsPerWarp; ++k) {
@@ -873,10 +898,16 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
             const int c = warp + h * kWarpsBY;
             const int row = (q == 2) ? x0 + c : img_h - 1 - (x0 + c);
             const In* __restrict__ rp = im + (size_t)row * img_pitch;
+            if (s0 + R <= H) {  // no wrap in this row tile
 #pragma unroll
-            for (int k = 0; k < kRowsPerLane; ++k) {
-                const int i = lane + 32 * k;
-                if (i < R) v[h][k] = rp[wrap_any(s0 + i, H)];
+                for (int k = 0; k < kRowsPerLane; ++k)
+                    if (lane + 32 * k < R) v[h][k] = rp[s0 + lane + 32 * k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < kRowsPerLane; ++k) {
+                    const int i = lane + 32 * k;
+                    if (i < R) v[h][k] = rp[wrap_any(s0 + i, H)];
+                }
             }
         }
 #pragma unroll
