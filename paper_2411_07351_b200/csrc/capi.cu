@@ -285,15 +285,30 @@ void upload(Group& g) {
         {
             const int64_t L = g.pass_L[o_passes.size()], S = g.pass_S[o_passes.size()];
             std::vector<int4> bops;
-            if (g.pairs) {  // 2 records per op: {dst, rows, nterms, term0}, {term1, term2, term3, split}
-                for (const auto& op : ps.pops) {
+            if (g.pairs) {  // 2 records per op: {dst, rows, nterms | (gcol+1) << 3, term0}, {term1, term2, term3, split}
+                // ops of a tile's last step that produce a stored column carry
+                // its global column: non-root bands store them from registers
+                std::vector<int> gcol_of(ps.pops.size(), -1);
+                for (const auto& t : ps.ptiles) {
+                    if (t.nsteps == 0) continue;
+                    const int lo = ps.pstep_offs[static_cast<size_t>(t.step_beg + t.nsteps - 1)];
+                    const int hi = ps.pstep_offs[static_cast<size_t>(t.step_beg + t.nsteps)];
+                    for (int o = lo; o < hi; ++o)
+                        for (int k = 0; k < t.store_cnt; ++k) {
+                            const auto& st = ps.pstores[static_cast<size_t>(t.store_beg + k)];
+                            if (st.slot == ps.pops[static_cast<size_t>(o)].dst) gcol_of[static_cast<size_t>(o)] = st.gcol;
+                        }
+                }
+                for (size_t oi = 0; oi < ps.pops.size(); ++oi) {
+                    const auto& op = ps.pops[oi];
                     int64_t t[4] = {0, 0, 0, 0};
                     for (int k = 0; k < op.nterms; ++k) t[k] = (op.term[k].slot * L + op.term[k].off) * 4;
                     const int64_t d = op.dst * L * 4;
                     if (d > INT32_MAX || *std::max_element(t, t + 4) > INT32_MAX)
                         throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
-                    bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(S + op.ext), op.nterms,
-                                             static_cast<int>(t[0])));
+                    if (gcol_of[oi] >= (1 << 27)) throw FhtError(FHT_ERR_INTERNAL, "column index overflow");
+                    bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(S + op.ext),
+                                             op.nterms | ((gcol_of[oi] + 1) << 3), static_cast<int>(t[0])));
                     bops.push_back(make_int4(static_cast<int>(t[1]), static_cast<int>(t[2]), static_cast<int>(t[3]), op.split));
                 }
             }

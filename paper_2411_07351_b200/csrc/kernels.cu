@@ -259,20 +259,58 @@ __device__ __forceinline__ void rows_op_terms(uint32_t d, const uint32_t (&t)[4]
         }
 }
 
-template <class Acc, int NWARPS>
+// A stored column of a non-root band written straight to the workspace
+// from registers (lane = row: 128 contiguous bytes per warp store).
+template <class Acc, int K, int SPLIT>
+__device__ __forceinline__ void rows_op_terms_global(Acc* __restrict__ g, const uint32_t (&t)[4], int n, int lane) {
+    constexpr int U = 4;
+    const uint32_t lo = lane * 4u;
+    int i0 = 0;
+    for (; i0 + 32 * U <= n; i0 += 32 * U) {
+        int v[U][4];
+        const uint32_t o = lo + i0 * 4u;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) g[i0 + 32 * u + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v[u]));
+    }
+    for (; i0 < n; i0 += 32)
+        if (i0 + lane < n) {
+            const uint32_t o = lo + i0 * 4u;
+            int v[4];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + o);
+            g[i0 + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v));
+        }
+}
+
+template <class Acc, int NWARPS, bool DIRECT>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
-                                               int warp, int lane) {
+                                               int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
+                                               int rows_out = 0) {
     for (int o = o_beg + warp; o < o_end; o += NWARPS) {
         const int4 h = ops[2 * o], q = ops[2 * o + 1];
         const uint32_t d = base + static_cast<uint32_t>(h.x);
         const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
                                base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
-        const int n = h.y;
-        if (h.z == 4) {
+        const int n = h.y, nt = h.z & 7, gc = (h.z >> 3) - 1;
+        if (DIRECT && gdst != nullptr && gc >= 0) {  // a stored column (non-root band): straight to the workspace
+            Acc* __restrict__ g = gdst + (size_t)gc * ld;
+            if (nt == 4) rows_op_terms_global<Acc, 4, 2>(g, t, rows_out, lane);
+            else if (nt == 2) rows_op_terms_global<Acc, 2, 1>(g, t, rows_out, lane);
+            else if (nt == 3 && q.w == 2) rows_op_terms_global<Acc, 3, 2>(g, t, rows_out, lane);
+            else if (nt == 3) rows_op_terms_global<Acc, 3, 1>(g, t, rows_out, lane);
+            else
+                for (int i = lane; i < rows_out; i += 32) g[i] = from_bits<Acc>(lds1u(t[0] + 4u * i));
+            continue;
+        }
+        if (nt == 4) {
             rows_op_terms<Acc, 4, 2>(d, t, n, lane);
-        } else if (h.z == 2) {
+        } else if (nt == 2) {
             rows_op_terms<Acc, 2, 1>(d, t, n, lane);
-        } else if (h.z == 3) {
+        } else if (nt == 3) {
             if (q.w == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
             else rows_op_terms<Acc, 3, 1>(d, t, n, lane);
         } else {  // a single term: copy
@@ -1069,7 +1107,8 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
 
 
 // MODE 0: one level per step, 4 rows per lane; 1: rows interleaved over
-// lanes; 2: level-pair programs (4-byte accumulators only).
+// lanes; 2: level-pair programs (4-byte accumulators only); 4: level pairs of
+// a non-root band, its last step storing the band's columns from registers.
 template <class Acc, class Out, int MODE>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
@@ -1091,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     int* ssteps = reinterpret_cast<int*>(sops + ps.max_tile_ops);  // the tile's step offsets (after the ops)
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid];
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
-    if constexpr (MODE == 2) {
+    if constexpr (MODE == 2 || MODE == 4) {
         for (int k = tid; k < 2 * nops; k += kThreads2) sbops[k] = ps.bops[2 * op0 + k];
     } else if constexpr (sizeof(Acc) == 4) {
         for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
@@ -1129,8 +1168,15 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
-        if constexpr (MODE == 2)
-            run_step_terms<Acc, kWarps>(sbase, sbops, ob, oe, warp, lane);
+        if constexpr (MODE == 2) {
+            run_step_terms<Acc, kWarps, false>(sbase, sbops, ob, oe, warp, lane);
+        } else if constexpr (MODE == 4) {
+            // the last step of a non-root band stores its columns from registers
+            const bool direct = k + 1 == tile.nsteps;
+            run_step_terms<Acc, kWarps, true>(sbase, sbops, ob, oe, warp, lane,
+                                              direct ? dst + (size_t)slot * slot_elems + s0 : nullptr, ld,
+                                              min(S, H - s0));
+        }
         else if constexpr (sizeof(Acc) == 4)
             run_step_baked<Acc, kWarps, MODE == 1>(sbase, sbops, ob, oe, warp, lane);
         else
@@ -1139,6 +1185,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     __syncthreads();
     // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)
     const int rows = min(S, H - s0);
+    if (MODE == 4 && tile.nsteps > 0) return;  // stored by the last step
     if (!final_pass) {
         Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
         const bool al = ((ld | s0) & 3) == 0;
@@ -1354,7 +1401,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
         auto k2 = k2_pass<Acc, Out, 0>;
         if constexpr (sizeof(Acc) == 4) {
-            if (ps.pairs) k2 = k2_pass<Acc, Out, 2>;
+            // level pairs; non-root bands (MODE 4) store their columns from registers
+            if (ps.pairs) k2 = final_pass ? k2_pass<Acc, Out, 2> : k2_pass<Acc, Out, 4>;
             else if (g.k2_scalar) k2 = k2_pass<Acc, Out, 1>;
         }
         PassDev pd = ps;
