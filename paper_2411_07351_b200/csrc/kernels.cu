@@ -583,30 +583,47 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
     if (c >= w) c = c - w < w ? c - w : c % w;
     const unsigned char* __restrict__ src = img + (size_t)(img0 + im) * img_stride + c;
     unsigned char v[16];
+    if (r0 + 64 <= h) {  // no wrapped rows in this tile: one pointer, fixed stride
+        const unsigned char* __restrict__ p = src + (size_t)(r0 + ty) * pitch;
+        const size_t step = 4 * (size_t)pitch;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        int r = r0 + ty + 4 * k;
-        if (r >= h) r = r - h < h ? r - h : r % h;
-        v[k] = src[(size_t)r * pitch];
+        for (int k = 0; k < 16; ++k) v[k] = p[k * step];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            int r = r0 + ty + 4 * k;
+            if (r >= h) r = r - h < h ? r - h : r % h;  // the wrapped head rows
+            v[k] = src[(size_t)r * pitch];
+        }
     }
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[ty + 4 * k][tx] = v[k];
     __syncthreads();
     unsigned char* __restrict__ dst = st + (size_t)im * simg;
-    const int j = threadIdx.x & 15;  // 16 words of 4
-    if (want_t) {  // word j of T row x = c0 + cc: rows r0 + 4j .. + 3
+    if (want_t) {
+        // thread = a 4 x 4 byte block (rows 4j.., columns 4i..): four aligned
+        // word reads, a byte transpose, four T words (lanes along j: each
+        // group of 16 lanes writes 64 contiguous bytes of one T column)
+        const int j = threadIdx.x & 15, i = threadIdx.x >> 4;
+        const uint32_t a = *reinterpret_cast<const uint32_t*>(&tile[4 * j][4 * i]);
+        const uint32_t b = *reinterpret_cast<const uint32_t*>(&tile[4 * j + 1][4 * i]);
+        const uint32_t cc = *reinterpret_cast<const uint32_t*>(&tile[4 * j + 2][4 * i]);
+        const uint32_t d = *reinterpret_cast<const uint32_t*>(&tile[4 * j + 3][4 * i]);
+        const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+        const uint32_t t2 = __byte_perm(cc, d, 0x5140), t3 = __byte_perm(cc, d, 0x7362);
+        const uint32_t col[4] = {__byte_perm(t0, t2, 0x5410), __byte_perm(t0, t2, 0x7632), __byte_perm(t1, t3, 0x5410),
+                                 __byte_perm(t1, t3, 0x7632)};
         const long long y = r0 + 4 * j;
+        if (y < pitch_t) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int cc = (threadIdx.x >> 4) + 16 * k, x = c0 + cc;
-            if (x < w && y < pitch_t) {
-                const uint32_t word = tile[4 * j][cc] | (tile[4 * j + 1][cc] << 8) | (tile[4 * j + 2][cc] << 16) |
-                                      (static_cast<uint32_t>(tile[4 * j + 3][cc]) << 24);
-                *reinterpret_cast<uint32_t*>(dst + off_t + (size_t)x * pitch_t + y) = word;
+            for (int m = 0; m < 4; ++m) {
+                const int x = c0 + 4 * i + m;
+                if (x < w) *reinterpret_cast<uint32_t*>(dst + off_t + (size_t)x * pitch_t + y) = col[m];
             }
         }
     }
     if (want_p) {  // word j of P row r = r0 + rr: columns c0 + 4j .. + 3
+        const int j = threadIdx.x & 15;
         const long long y = c0 + 4 * j;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
