@@ -30,7 +30,7 @@ namespace fhtb {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ int wrap_once(int j, int H) { return j >= H ? j - H : j; }
