@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--strategy", default="tweaked", choices=["simple", "tweaked"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay one captured CUDA graph per step instead of launching through the API "
+                         "(measured: no gain; programmatic dependent launch already hides the gaps)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -273,8 +276,13 @@ def run_ours(args):
     if root_split is not None:
         rs_backend = shard.GpuRootBackend(strategy, c.dtype, c.acc)
 
+    graph = None
+
     def step():
         if my_q is None:
+            return
+        if graph is not None:
+            graph.replay()
             return
         if root_split is not None:
             shard.root_split_quadrant(x[0], my_q[0], strategy, side=root_split[0], backend=rs_backend,
@@ -290,6 +298,22 @@ def run_ours(args):
         flush.fill_(1)
         step()
     torch.cuda.synchronize()
+    if args.graph and my_q is not None and root_split is None:
+        # one execute (all its launches, the auxiliary-stream fork/join and the
+        # programmatic launch edges) captured once and replayed per step
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            check(lib().fht_execute(plan._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
+                                    ctypes.c_void_p(wsbuf.data_ptr() if wsbuf is not None else 0),
+                                    ctypes.c_void_p(cap.cuda_stream)))
+        torch.cuda.synchronize()
+        graph = g
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            step()
+        torch.cuda.synchronize()
     t_soak = time.perf_counter()
     while time.perf_counter() - t_soak < 0.5:  # untimed soak: clocks settle under load
         for _ in range(8):
@@ -417,6 +441,7 @@ def run_ours(args):
             "data": "synthetic (seeded, BASELINE.json config shapes/distributions)",
             "config": {"workload": args.config, "description": c.description, "n": c.n,
                        "images_per_gpu": c.batch, "quadrants": len(c.quadrants), "strategy": args.strategy,
+                       "cuda_graph": graph is not None,
                        "in_dtype": c.dtype, "acc_dtype": c.acc,
                        "parallelism": (("root-split x2 per quadrant" if ws > len(c.quadrants) else f"quadrant-split x{ws}")
                                        if scaling == "strong" else f"batch-shard x{ws}"),
