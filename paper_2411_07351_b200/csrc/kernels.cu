@@ -1100,21 +1100,45 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
             // 16-byte copies while both sides are 16-byte aligned, 4-byte after
             const int na = min(n, H - start);
             const int run = (start & 3) ? 0 : (na & ~3);
+            // copy loops advance a global pointer and a shared offset (no
+            // per-copy 64-bit index arithmetic), two copies per iteration
             if (bar) {  // aligned runs by the TMA engine, the rest 4-byte
                 if (lane == 0 && run > 0) bulk_copy(d, col + start, run * 4u, bar);
             } else {
-                for (int k = lane; 4 * k < run; k += 32) cp_async16(d + 16u * k, col + start + 4 * k);
+                const Acc* g = col + start + 4 * lane;
+                uint32_t sd = d + 16u * lane;
+                int k = lane;
+                for (; 4 * (k + 32) < run; k += 64, g += 256, sd += 1024u) {
+                    cp_async16(sd, g);
+                    cp_async16(sd + 512u, g + 128);
+                }
+                if (4 * k < run) cp_async16(sd, g);
             }
-            for (int i = run + lane; i < na; i += 32) cp_async4(d + 4u * i, col + start + i);
+            {
+                const Acc* g = col + start + run + lane;
+                uint32_t sd = d + 4u * (run + lane);
+                int i = run + lane;
+                for (; i + 32 < na; i += 64, g += 64, sd += 256u) {
+                    cp_async4(sd, g);
+                    cp_async4(sd + 128u, g + 32);
+                }
+                if (i < na) cp_async4(sd, g);
+            }
             if (n - na <= H) {
-                const Acc* cb = col - na;  // rows past the wrap point: col[i - na]
-                int i0 = na;
+                int i0 = na;  // rows past the wrap point: col[i - na]
                 if (bar && (na & 3) == 0) {
                     const int nb = (n - na) & ~3;
                     if (lane == 0 && nb > 0) bulk_copy(d + 4u * na, col, nb * 4u, bar);
                     i0 += nb;
                 }
-                for (int i = i0 + lane; i < n; i += 32) cp_async4(d + 4u * i, cb + i);
+                const Acc* g = col + (i0 - na) + lane;
+                uint32_t sd = d + 4u * (i0 + lane);
+                int i = i0 + lane;
+                for (; i + 32 < n; i += 64, g += 64, sd += 256u) {
+                    cp_async4(sd, g);
+                    cp_async4(sd + 128u, g + 32);
+                }
+                if (i < n) cp_async4(sd, g);
             } else {  // a window longer than the column (tiny H): wraps again
                 for (int i = na + lane; i < n; i += 32) cp_async4(d + 4u * i, col + wrap_any(i - na, H));
             }
