@@ -399,9 +399,15 @@ def run_ours(args):
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            tr = json.loads(prof.read_text()).get(args.config, {}).get(names[dom])
+            pj = json.loads(prof.read_text())
+            tr = pj.get(args.config, {}).get(names[dom])
             if tr:
                 roofline["traffic"] = tr
+            # what actually binds the kernel (ncu, same capture): LSU/shared
+            # data-pipe wavefronts and issue slots, as fractions of peak
+            lsu = pj.get("lsu_issue", {}).get(args.config, {}).get(names[dom])
+            if lsu:
+                roofline["lsu_pipe_frac_ncu"], roofline["issue_frac_ncu"] = lsu
         except Exception:
             pass
 

@@ -28,7 +28,9 @@ def main(rep, top=25):
             if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "smsp__inst_executed.sum",
                      "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
                      "sm__sass_inst_executed_op_shared_ld.sum", "sm__sass_inst_executed_op_shared_st.sum",
-                     "sm__sass_inst_executed_op_global_ld.sum", "gpu__time_duration.sum"):
+                     "sm__sass_inst_executed_op_global_ld.sum", "gpu__time_duration.sum",
+                     "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                     "smsp__issue_active.avg.pct_of_peak_sustained_active"):
                 print(f"raw   {k} = {v} {u}")
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
