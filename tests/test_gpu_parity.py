@@ -253,6 +253,31 @@ def test_execute_host_roundtrip():
             np.testing.assert_array_equal(out[k][bi], ref[k])
 
 
+@pytest.mark.parametrize("stage,parts,chunk", [(1, 3, None), (1, 1, 5), (0, 4, 3)])
+def test_execute_host_parts_and_chunks(monkeypatch, stage, parts, chunk):
+    """The host-buffer path cuts a batch into parts on three streams, each with
+    its own workspace slice; with u8 staging the staged columns live after a
+    chunk's slot buffers.  Every image must match the oracle (and the device
+    path) whatever the part/chunk split."""
+    monkeypatch.setenv("FHT_K1_STAGE", str(stage))
+    monkeypatch.setenv("FHT_HOST_PARTS", str(parts))
+    if chunk:
+        monkeypatch.setenv("FHT_CHUNK_IMAGES", str(chunk))
+    rng = np.random.default_rng(13)
+    n, b = 509, 11
+    imgs = rng.integers(0, 256, (b, n, n), dtype=np.uint8)
+    plan = fht.Plan(n, n, 1, in_dtype="u8", acc_dtype="i32", batch=b)
+    assert (plan.describe()["groups"][0]["stage_bytes"] > 0) == bool(stage)
+    host = plan.execute_host(imgs)
+    dev, _ = run_plan(imgs, "u8", "i32", 1)
+    for bi in (0, 4, b - 1):
+        ref, _ = oracle.fht2d_quadrants(imgs[bi], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(host[k][bi], ref[k], err_msg=f"host img{bi} {k}")
+    for k in Q:
+        np.testing.assert_array_equal(host[k], dev[k])
+
+
 def test_profiled_launch_accounting(monkeypatch):
     """fht_execute_profiled: one record per launch, kinds in launch order and
     algorithmic bytes that add up to the plan's passes (bench roofline input)."""
