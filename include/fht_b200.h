@@ -110,6 +110,27 @@ int fht_execute(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void
 int fht_execute_pitched(fht_plan_t plan, const void* d_in, int64_t in_row_pitch, int64_t in_image_stride,
                         void* const d_out[4], int64_t out_image_stride, void* d_workspace, void* stream);
 
+/* fht_execute_pitched for the multi-GPU root split, with the exchange fused
+ * into the transform: a one-image, one-quadrant FHT_LAYOUT_NATIVE plan whose
+ * last pass also stores slopes [peer_first, peer_end) of its output to
+ * d_peer + (t - peer_first) * H -- typically the other GPU's receive buffer,
+ * mapped with fht_ipc_open_handle, written over NVLink as the tiles finish
+ * (no separate send/recv).  d_peer = NULL: plain fht_execute_pitched. */
+int fht_execute_pitched_peer(fht_plan_t plan, const void* d_in, int64_t in_row_pitch, void* const d_out[4],
+                             void* d_workspace, void* d_peer, int peer_first, int peer_end, void* stream);
+
+/* CUDA IPC for the fused exchange: export a device allocation as an opaque
+ * handle (FHT_IPC_HANDLE_BYTES), open another process's handle on `device`
+ * (peer access enabled on demand), close a mapping. */
+#define FHT_IPC_HANDLE_BYTES 64
+/* A dedicated cudaMalloc allocation (an IPC handle covers a whole allocation,
+ * so exported buffers must not be sub-allocated). */
+int fht_device_alloc(size_t bytes, int device, void** d_ptr);
+int fht_device_free(void* d_ptr);
+int fht_ipc_get_handle(const void* d_ptr, void* handle, size_t handle_len);
+int fht_ipc_open_handle(const void* handle, size_t handle_len, int device, void** d_ptr);
+int fht_ipc_close(void* d_ptr);
+
 /* The root level of a width-W, H-shift transform from its two children, each
  * given as a slope-major column range (the FHT_LAYOUT_NATIVE output of a plan
  * over that child's columns): left child slopes [left_first, ...) at d_left,
@@ -124,8 +145,8 @@ int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_d
 
 /* fht_execute with a CUDA event recorded after every kernel launch on
  * `stream`; synchronises and returns each launch's duration (ms), kind
- * (1 = K1 generic blocks, 4 = K1P width-32 Brady-Yong blocks, 2 = K2 fused
- * upper pass, 3 = K2 root pass) and algorithmic bytes (each input cell read
+ * (5 = u8 staging, 1 = K1 generic blocks, 4 = K1P width-32 Brady-Yong blocks,
+ * 2 = K2 fused upper pass, 3 = K2 root pass) and algorithmic bytes (each input cell read
  * once, each output cell written once).  For the bench's live per-kernel
  * roofline. */
 int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_stride, void* const d_out[4],

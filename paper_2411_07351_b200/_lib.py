@@ -37,6 +37,12 @@ SIGNATURES = {
     "fht_execute_host": (_i, [_vp, _vp, ctypes.POINTER(_vp), _vp]),
     "fht_execute_pitched": (_i, [_vp, _vp, _i64, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp]),
     "fht_merge_root": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _i, _i, _i, _vp, _vp]),
+    "fht_execute_pitched_peer": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _vp, _vp, _i, _i, _vp]),
+    "fht_ipc_get_handle": (_i, [_vp, _vp, ctypes.c_size_t]),
+    "fht_ipc_open_handle": (_i, [_vp, ctypes.c_size_t, _i, ctypes.POINTER(_vp)]),
+    "fht_ipc_close": (_i, [_vp]),
+    "fht_device_alloc": (_i, [ctypes.c_size_t, _i, ctypes.POINTER(_vp)]),
+    "fht_device_free": (_i, [_vp]),
     "fht_execute_profiled": (_i, [_vp, _vp, _i64, ctypes.POINTER(_vp), _i64, _vp, _vp, ctypes.POINTER(ctypes.c_float),
                                   _pi, ctypes.POINTER(ctypes.c_double), _i, _pi]),
     "fht_check_budget": (_i, [_vp, _i, _i64, _i, _pi, _vp]),

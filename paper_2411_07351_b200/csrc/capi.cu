@@ -522,9 +522,14 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     return p.release();
 }
 
+struct PeerOut {  // fht_execute_pitched_peer: slopes [c0, c1) also stored to `ptr`
+    void* ptr = nullptr;
+    int c0 = 0, c1 = 0;
+};
+
 void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_out[4], int64_t out_stride,
              void* ws, cudaStream_t st, fhtb::LaunchHook hook = nullptr, void* ctx = nullptr, int64_t in_pitch = 0,
-             int img_begin = 0, int img_end = -1) {
+             int img_begin = 0, int img_end = -1, PeerOut peer = {}) {
     if (img_end < 0) img_end = p->batch;
     if (in_pitch == 0) in_pitch = p->w;
     if (in_pitch < p->w) throw std::invalid_argument("fht_execute: row pitch smaller than the image width");
@@ -588,6 +593,9 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.out.img_stride = out_stride;
             L.out.layout = p->layout;
             L.out.dtype = p->out;
+            L.out.peer = peer.ptr;
+            L.out.peer_c0 = peer.c0;
+            L.out.peer_c1 = peer.c1;
             if (fhtb::launch_group(L, st, hook, ctx) < 0) throw FhtError(FHT_ERR_INVALID, "unsupported dtype triple");
             cuda_check(cudaGetLastError(), "kernel launch");
         }
@@ -861,6 +869,62 @@ int fht_execute_pitched(fht_plan_t plan, const void* d_in, int64_t in_row_pitch,
         execute(plan, d_in, in_image_stride, d_out, out_image_stride, d_workspace, static_cast<cudaStream_t>(stream),
                 nullptr, nullptr, in_row_pitch);
     });
+}
+
+int fht_execute_pitched_peer(fht_plan_t plan, const void* d_in, int64_t in_row_pitch, void* const d_out[4],
+                             void* d_workspace, void* d_peer, int peer_first, int peer_end, void* stream) {
+    return guarded([&] {
+        if (!plan || !d_out) throw std::invalid_argument("fht_execute_pitched_peer: null argument");
+        if (plan->layout != FHT_LAYOUT_NATIVE || plan->batch != 1 || plan->groups.size() != 1 ||
+            plan->groups[0]->qs.n != 1)
+            throw std::invalid_argument("fht_execute_pitched_peer: needs a one-image, one-quadrant, native-layout plan");
+        const int W = plan->groups[0]->sp.W;
+        if (d_peer && (peer_first < 0 || peer_end > W || peer_first > peer_end))
+            throw std::invalid_argument("fht_execute_pitched_peer: bad slope range");
+        PeerOut peer;
+        peer.ptr = d_peer;
+        peer.c0 = peer_first;
+        peer.c1 = peer_end;
+        execute(plan, d_in, 0, d_out, 0, d_workspace, static_cast<cudaStream_t>(stream), nullptr, nullptr, in_row_pitch,
+                0, -1, peer);
+    });
+}
+
+int fht_device_alloc(size_t bytes, int device, void** d_ptr) {
+    return guarded([&] {
+        if (!d_ptr) throw std::invalid_argument("fht_device_alloc: null pointer");
+        DeviceGuard dg(device);
+        cuda_check(cudaMalloc(d_ptr, std::max<size_t>(bytes, 1)), "cudaMalloc");
+    });
+}
+
+int fht_device_free(void* d_ptr) {
+    return guarded([&] { cuda_check(cudaFree(d_ptr), "cudaFree"); });
+}
+
+int fht_ipc_get_handle(const void* d_ptr, void* handle, size_t handle_len) {
+    return guarded([&] {
+        if (!d_ptr || !handle || handle_len < sizeof(cudaIpcMemHandle_t))
+            throw std::invalid_argument("fht_ipc_get_handle: null pointer or short buffer");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof(h));
+    });
+}
+
+int fht_ipc_open_handle(const void* handle, size_t handle_len, int device, void** d_ptr) {
+    return guarded([&] {
+        if (!handle || !d_ptr || handle_len < sizeof(cudaIpcMemHandle_t))
+            throw std::invalid_argument("fht_ipc_open_handle: null pointer or short buffer");
+        DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        cuda_check(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int fht_ipc_close(void* d_ptr) {
+    return guarded([&] { cuda_check(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle"); });
 }
 
 int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_dtype, int layout, const void* d_left,

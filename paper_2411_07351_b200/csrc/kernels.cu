@@ -552,8 +552,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
             for (int i = warp; i < rows_out; i += kWarps)
                 for (int c = lane; c < wb; c += 32) o[(size_t)(s0 + i) * W + c] = static_cast<Out>(buf0[c * sr + i]);
         } else {
-            for (int c = warp; c < wb; c += kWarps)
-                for (int i = lane; i < rows_out; i += 32) o[(size_t)c * H + s0 + i] = static_cast<Out>(buf0[c * sr + i]);
+            Out* __restrict__ pr = static_cast<Out*>(out.peer);
+            for (int c = warp; c < wb; c += kWarps) {
+                const bool to_peer = pr != nullptr && c >= out.peer_c0 && c < out.peer_c1;
+                for (int i = lane; i < rows_out; i += 32) {
+                    const Out v = static_cast<Out>(buf0[c * sr + i]);
+                    o[(size_t)c * H + s0 + i] = v;
+                    if (to_peer) pr[(size_t)(c - out.peer_c0) * H + s0 + i] = v;  // NVLink store
+                }
+            }
         }
     }
 }
@@ -1290,10 +1297,22 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
                 }
             }
         } else {
+            Out* __restrict__ pr = static_cast<Out*>(out.peer);
             for (int c = warp; c < nc; c += kWarps) {
                 const int2 st = ps.stores[tile.store_beg + c];
                 const Acc* sv = sm + (size_t)st.x * L;
                 Out* __restrict__ dcol = o + (size_t)st.y * H + s0;
+                if (pr != nullptr && st.y >= out.peer_c0 && st.y < out.peer_c1) {
+                    // a slope the other side of the root split needs: also
+                    // stored straight into its buffer (peer memory over NVLink)
+                    Out* __restrict__ pcol = pr + (size_t)(st.y - out.peer_c0) * H + s0;
+                    for (int i = lane; i < rows; i += 32) {
+                        const Out v = static_cast<Out>(sv[i]);
+                        dcol[i] = v;
+                        pcol[i] = v;
+                    }
+                    continue;
+                }
                 for (int i = lane; i < rows; i += 32) dcol[i] = static_cast<Out>(sv[i]);
             }
         }

@@ -28,6 +28,11 @@ struct OutDesc {
     long long img_stride;
     int layout;
     int dtype;
+    // slope-major (native) layout only: slopes [peer_c0, peer_c1) are also
+    // stored to peer + (t - peer_c0) * H -- another GPU's buffer mapped over
+    // NVLink (the root split's exchange, fused into the child's last pass)
+    void* peer;
+    int peer_c0, peer_c1;
 };
 
 // Per K1 shape header (8 ints): width, nsteps, op_base, step_base, halo.

@@ -5,12 +5,17 @@ the data path.
   contiguous, balanced shard of the batch (`batch_shard`).
 * One large image (config c5): the four quadrants are independent -> rank r
   transforms the quadrants assigned to it (`quadrant_shard`).
+* One large image on 8 ranks (c5): two GPUs per quadrant split its root
+  (`root_split_quadrant`); the one exchange is fused into the child
+  transform, whose last pass stores the slopes the peer needs straight into
+  the peer's buffer over NVLink (`PeerExchange`, CUDA IPC), NCCL/gloo
+  send/recv as the fallback.
 * Results may optionally be gathered to rank 0 with one collective
-  (`gather_to_root`, NCCL on GPUs, gloo in the CPU tests).  The transform
-  itself never communicates.
+  (`gather_to_root`, NCCL on GPUs, gloo in the CPU tests).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 QUADRANTS = ("horiz_pos", "horiz_neg", "vert_pos", "vert_neg")
@@ -126,7 +131,7 @@ class GpuRootBackend:
         self.layout = layout
         self._plans = {}
 
-    def child(self, view, quadrant: str, side: int = 0):
+    def child(self, view, quadrant: str, side: int = 0, peer_ptr: int | None = None, peer_cols=(0, 0)):
         import ctypes
 
         import torch
@@ -144,10 +149,24 @@ class GpuRootBackend:
         ptrs = (ctypes.c_void_p * 4)()
         ptrs[fht.QUADRANTS.index(quadrant)] = out[quadrant].data_ptr()
         st = torch.cuda.current_stream(view.device)
-        check(lib().fht_execute_pitched(plan._h, ctypes.c_void_p(view.data_ptr()), view.stride(0), 0, ptrs, 0,
-                                        ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
-                                        ctypes.c_void_p(st.cuda_stream)))
+        wsp = ctypes.c_void_p(ws.data_ptr() if ws is not None else 0)
+        if peer_ptr:  # the exchange fused into the last pass: peer slopes stored over NVLink
+            check(lib().fht_execute_pitched_peer(plan._h, ctypes.c_void_p(view.data_ptr()), view.stride(0), ptrs, wsp,
+                                                 ctypes.c_void_p(peer_ptr), int(peer_cols[0]), int(peer_cols[1]),
+                                                 ctypes.c_void_p(st.cuda_stream)))
+        else:
+            check(lib().fht_execute_pitched(plan._h, ctypes.c_void_p(view.data_ptr()), view.stride(0), 0, ptrs, 0, wsp,
+                                            ctypes.c_void_p(st.cuda_stream)))
         return out[quadrant][0]  # (child width, H) slope-major
+
+    def peer_exchange(self, key, nbytes: int, device: int, peer: int, group=None) -> "PeerExchange":
+        """The receive buffer this side exposes to its root-split peer and the
+        peer's buffer mapped here (CUDA IPC over NVLink), built once per key."""
+        if not hasattr(self, "_peers"):
+            self._peers = {}
+        if key not in self._peers:
+            self._peers[key] = PeerExchange(nbytes, device, peer, group)
+        return self._peers[key]
 
     def merge(self, split: RootSplit, left, left_first, right, right_first, t_beg, t_end, out):
         import ctypes
@@ -158,11 +177,12 @@ class GpuRootBackend:
         from ._lib import check, lib
 
         st = torch.cuda.current_stream(out.device)
+        lp = left if isinstance(left, int) else left.data_ptr()  # tensors, or raw device pointers
+        rp = right if isinstance(right, int) else right.data_ptr()
         check(lib().fht_merge_root(split.W, split.H, fht._strategy(self.strategy), fht._dtype_code(self.acc_dtype),
                                    fht._dtype_code(self.out_dtype), 0 if self.layout == "reference" else 1,
-                                   ctypes.c_void_p(left.data_ptr()), left_first, ctypes.c_void_p(right.data_ptr()),
-                                   right_first, t_beg, t_end, ctypes.c_void_p(out.data_ptr()),
-                                   ctypes.c_void_p(st.cuda_stream)))
+                                   ctypes.c_void_p(lp), left_first, ctypes.c_void_p(rp), right_first, t_beg, t_end,
+                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
 
     def empty_out(self, split: RootSplit, like):
         import torch
@@ -172,7 +192,43 @@ class GpuRootBackend:
         return torch.zeros(shape, dtype=dt, device=like.device)
 
 
-def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: int | None = None, group=None):
+class PeerExchange:
+    """One side's half of the fused root-split exchange: a dedicated device
+    buffer the peer writes its child slopes into (exported as a CUDA IPC
+    handle), and the peer's buffer opened here.  Handles travel once over the
+    process group (any backend); the data never does -- the child transform's
+    last pass stores it straight into peer memory over NVLink."""
+
+    def __init__(self, nbytes: int, device: int, peer: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from ._lib import check, lib
+
+        self.local = ctypes.c_void_p()
+        check(lib().fht_device_alloc(max(1, nbytes), device, ctypes.byref(self.local)))
+        handle = ctypes.create_string_buffer(64)
+        check(lib().fht_ipc_get_handle(self.local, handle, 64))
+        got = [None] * dist.get_world_size(group)
+        dist.all_gather_object(got, (dist.get_rank(), handle.raw), group=group)
+        peer_handle = dict(got)[peer]
+        self.remote = ctypes.c_void_p()
+        check(lib().fht_ipc_open_handle(peer_handle, 64, device, ctypes.byref(self.remote)))
+
+    def close(self):
+        from ._lib import lib
+
+        if self.remote:
+            lib().fht_ipc_close(self.remote)
+            self.remote = None
+        if self.local:
+            lib().fht_device_free(self.local)
+            self.local = None
+
+
+def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: int | None = None, group=None,
+                        exchange: str | None = None):
     """One side of the two-GPU root split of `quadrant` of `img` (the whole
     image, resident on this rank).  `peer` is the other side's global rank
     (None: both sides run in this process, `side` ignored -- used to test the
@@ -191,12 +247,33 @@ def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: 
         out = backend.empty_out(sp, left)
         backend.merge(sp, left, 0, right, 0, 0, W, out)
         return out, sp
+    lo, hi = sp.left_for_1 if side == 0 else sp.right_for_0
+    rlo, rhi = sp.right_for_0 if side == 0 else sp.left_for_1
+    exchange = exchange or os.environ.get("FHT_ROOT_EXCHANGE", "p2p")
+    if exchange == "p2p" and img.is_cuda and hasattr(backend, "peer_exchange"):
+        # The exchange fused into the child transform: its last pass stores
+        # the slopes the peer needs straight into the peer's buffer (CUDA IPC
+        # mapping, NVLink stores); two barriers order the steps.
+        dev = img.device.index or 0
+        esz = torch.empty((), dtype={"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[backend.acc_dtype]
+                          ).element_size()
+        ex = backend.peer_exchange((quadrant, side, W, H), max(rhi - rlo, hi - lo) * H * esz, dev, peer, group)
+        torch.cuda.current_stream(img.device).synchronize()
+        dist.barrier(group)  # the peer is done reading its buffer from the previous step
+        mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side, peer_ptr=ex.remote.value,
+                             peer_cols=(lo, hi))
+        torch.cuda.current_stream(img.device).synchronize()
+        dist.barrier(group)  # both sides' peer stores have landed
+        out = backend.empty_out(sp, mine)
+        if side == 0:
+            backend.merge(sp, mine, 0, ex.local.value, rlo, 0, sp.t_mid, out)
+        else:
+            backend.merge(sp, ex.local.value, rlo, mine, 0, sp.t_mid, W, out)
+        return out, sp
     mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side)
     # gloo moves host tensors only: stage the exchange through host memory
     # (NCCL exchanges device buffers directly over NVLink)
     host = dist.get_backend(group) == "gloo" and mine.device.type == "cuda"
-    lo, hi = sp.left_for_1 if side == 0 else sp.right_for_0
-    rlo, rhi = sp.right_for_0 if side == 0 else sp.left_for_1
     send = mine[lo:hi].contiguous()
     recv = torch.empty((rhi - rlo, H), dtype=mine.dtype, device=mine.device)
     send_x, recv_x = (send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)) if host else (send, recv)

@@ -29,10 +29,10 @@ def _port():
     return p
 
 
-def _root_worker(rank, port, out):
+def _root_worker(rank, port, out, exchange):
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FHT_ROOT_EXCHANGE=exchange)
     dist.init_process_group("gloo", rank=rank, world_size=2)
     torch.cuda.set_device(0)
     sys.path.insert(0, str(ROOT))
@@ -41,20 +41,24 @@ def _root_worker(rank, port, out):
     rng = np.random.default_rng(9)
     img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
     be = shard.GpuRootBackend("tweaked", "f32", "f32")
-    res, sp = shard.root_split_quadrant(img, "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
+    for _ in range(2):  # twice: the receive buffers are reused across steps
+        res, sp = shard.root_split_quadrant(img, "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
     torch.cuda.synchronize()
     np.save(f"{out}.{rank}.npy", res.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_root_split_two_processes_one_gpu(tmp_path):
+@pytest.mark.parametrize("exchange", ["p2p", "sendrecv"])
+def test_root_split_two_processes_one_gpu(tmp_path, exchange):
+    """p2p: the children store the peer's slopes through a CUDA IPC mapping of
+    the peer process's buffer (the fused exchange); sendrecv: the fallback."""
     import torch.multiprocessing as mp
 
     from paper_2411_07351_b200 import fht, shard
 
     out = tmp_path / "rs"
-    mp.spawn(_root_worker, args=(_port(), str(out)), nprocs=2, join=True)
+    mp.spawn(_root_worker, args=(_port(), str(out), exchange), nprocs=2, join=True)
     rng = np.random.default_rng(9)
     img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
     full = fht.Plan(2049, 1500, "tweaked", in_dtype="f32", acc_dtype="f32", quadrants=["vert_pos"])(img[None])
