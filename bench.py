@@ -223,13 +223,15 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)  # before the process group: NCCL binds this rank to its GPU
+    dev = torch.device("cuda", local)
     if ws > 1:
         # NCCL across GPUs; FHT_DIST_BACKEND=gloo lets several ranks share one
         # GPU for functional testing (their kernels never wait on each other).
-        dist.init_process_group(os.environ.get("FHT_DIST_BACKEND", "nccl"), init_method="env://")
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        backend = os.environ.get("FHT_DIST_BACKEND", "nccl")
+        kw = {"device_id": dev} if backend == "nccl" else {}
+        dist.init_process_group(backend, init_method="env://", **kw)
     c = workloads.CONFIGS[args.config]
     strategy = 0 if args.strategy == "simple" else 1
 
@@ -315,11 +317,18 @@ def run_ours(args):
             step()
         torch.cuda.synchronize()
     t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < 0.5:  # untimed soak: clocks settle under load
+    while True:  # untimed soak: clocks settle under load
         for _ in range(8):
             flush.fill_(1)
             step()
         torch.cuda.synchronize()
+        go = time.perf_counter() - t_soak < 0.5
+        if ws > 1:  # every rank runs the same number of steps (the root split's steps are collective)
+            flag = torch.tensor([1 if go else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            go = bool(flag.item())
+        if not go:
+            break
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
