@@ -585,26 +585,36 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
     const bool want_t = off_t >= 0 && c0 < w && r0 < pitch_t;
     const bool want_p = off_p >= 0 && r0 < h && c0 < pitch_p;
     if (!want_t && !want_p) return;
-    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
-    int c = c0 + tx;
-    if (c >= w) c = c - w < w ? c - w : c % w;
-    const unsigned char* __restrict__ src = img + (size_t)(img0 + im) * img_stride + c;
-    unsigned char v[16];
-    if (r0 + 64 <= h) {  // no wrapped rows in this tile: one pointer, fixed stride
-        const unsigned char* __restrict__ p = src + (size_t)(r0 + ty) * pitch;
-        const size_t step = 4 * (size_t)pitch;
+    const unsigned char* __restrict__ base = img + (size_t)(img0 + im) * img_stride;
+    if (c0 + 64 <= w && r0 + 64 <= h) {
+        // interior tile: each row segment read as aligned 4-byte words (two
+        // per 4 pixels, funnel-shifted into place), 4 words per thread
+        const int j = threadIdx.x & 15, rr0 = threadIdx.x >> 4;  // word j of rows rr0, rr0 + 16, ...
+        uint32_t v[4];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = p[k * step];
+        for (int k = 0; k < 4; ++k) {
+            const unsigned char* p = base + (size_t)(r0 + rr0 + 16 * k) * pitch + c0 + 4 * j;
+            const uint32_t* a = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+            const uint32_t sh = 8u * static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) & 3);
+            v[k] = __funnelshift_r(__ldg(a), sh ? __ldg(a + 1) : 0u, sh);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(&tile[rr0 + 16 * k][4 * j]) = v[k];
     } else {
+        const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+        int c = c0 + tx;
+        if (c >= w) c = c - w < w ? c - w : c % w;
+        const unsigned char* __restrict__ src = base + c;
+        unsigned char v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             int r = r0 + ty + 4 * k;
             if (r >= h) r = r - h < h ? r - h : r % h;  // the wrapped head rows
             v[k] = src[(size_t)r * pitch];
         }
-    }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) tile[ty + 4 * k][tx] = v[k];
+        for (int k = 0; k < 16; ++k) tile[ty + 4 * k][tx] = v[k];
+    }
     __syncthreads();
     unsigned char* __restrict__ dst = st + (size_t)im * simg;
     if (want_t) {
