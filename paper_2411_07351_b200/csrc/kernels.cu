@@ -106,6 +106,13 @@ __device__ __forceinline__ void warp_merge(Acc* d, const Acc* a, const Acc* b, i
 __device__ __forceinline__ int quad_code(const QuadSet& qs, int i) {
     return i == 0 ? qs.code[0] : i == 1 ? qs.code[1] : i == 2 ? qs.code[2] : qs.code[3];
 }
+// slot = image * nq + quadrant index, nq in 1..4, without a runtime division
+__device__ __forceinline__ void split_slot(int slot, int nq, int& img, int& qi) {
+    if (nq == 4) img = slot >> 2, qi = slot & 3;
+    else if (nq == 2) img = slot >> 1, qi = slot & 1;
+    else if (nq == 1) img = slot, qi = 0;
+    else img = slot / 3, qi = slot - 3 * img;  // constant divisor
+}
 __device__ __forceinline__ void* out_ptr(const OutDesc& o, int q) {
     return q == 0 ? o.ptr[0] : q == 1 ? o.ptr[1] : q == 2 ? o.ptr[2] : o.ptr[3];
 }
@@ -459,8 +466,10 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
 
     const int slot = blockIdx.z;
     const int nq = qs.n;
-    const int img_i = img0 + slot / nq;
-    const int q = quad_code(qs, slot % nq);
+    int img_l, qi;
+    split_slot(slot, nq, img_l, qi);
+    const int img_i = img0 + img_l;
+    const int q = quad_code(qs, qi);
     const In* __restrict__ im = img + (size_t)img_i * img_stride;
     const int s0 = blockIdx.x * S;
 
@@ -665,6 +674,7 @@ constexpr int kBYW = 32;        // block width
 constexpr int kBYMaxS = 256;    // rows per tile (host guarantees S <= 256)
 constexpr int kBYSR = 300;      // slot stride: >= 256 + 31 + 12, multiple of 4, /4 odd
 constexpr int kThreadsBY = 512;
+static_assert(kThreadsBY == 8 * 64, "levels 1-2 map 8 column groups x 64 threads");
 constexpr int kWarpsBY = kThreadsBY / 32;
 
 // Level L (1..5) merges widths 2^(L-1) -> 2^L.  For block-local column T
@@ -802,8 +812,9 @@ __device__ __forceinline__ void by_level12(Acc* sm, int S, int tid) {
     const int4* V = reinterpret_cast<const int4*>(sm);
     int4* O = reinterpret_cast<int4*>(sm);
     constexpr int s4 = kBYSR / 4;
-    for (int it = tid; it < items; it += kThreadsBY) {
-        const int g = it / nchunk, j = it - g * nchunk;  // lanes over row chunks: conflict-free
+    (void)items;
+    const int g = tid >> 6;  // 8 column groups x 64 threads; lanes over row chunks: conflict-free
+    for (int j = tid & 63; j < nchunk; j += 64) {
         const int c0 = (kBYW + 4 * g) * s4 + j;  // leaves of column 4g, chunk j
         // pair (4g, 4g+1) -> level-1 columns p0 (shift 0), p1 (shift 1), rows j*4 .. j*4+6
         const int4 a0 = V[c0], a1 = V[c0 + 1], b0 = V[c0 + s4], b1 = V[c0 + s4 + 1];
@@ -840,8 +851,9 @@ __device__ __forceinline__ void by_level12_staged(Acc* sm, int S, int tid, const
     const int items = 8 * nchunk;
     int4* O = reinterpret_cast<int4*>(sm);
     constexpr int s4 = kBYSR / 4;
-    for (int it = tid; it < items; it += kThreadsBY) {
-        const int g = it / nchunk, j = it - g * nchunk;
+    (void)items;
+    const int g = tid >> 6;  // 8 column groups x 64 threads, lanes over consecutive row chunks
+    for (int j = tid & 63; j < nchunk; j += 64) {
         const int c = x0 + 4 * g;
         const long long cs = rev ? -spitch : spitch;  // reversed column order for horiz_neg / vert_neg
         const unsigned char* pa = sb + (long long)(rev ? W - 1 - c : c) * spitch + 4 * j;
@@ -881,8 +893,10 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     const int x0 = bx0[blockIdx.y];
     const int slot = blockIdx.z;
     const int nq = qs.n;
-    const int img_i = img0 + slot / nq;
-    const int q = quad_code(qs, slot % nq);
+    int img_l, qi;
+    split_slot(slot, nq, img_l, qi);
+    const int img_i = img0 + img_l;
+    const int q = quad_code(qs, qi);
     const In* __restrict__ im = img + (size_t)img_i * img_stride;
     const int s0 = blockIdx.x * S;
     const int R = S + kBYW - 1;
@@ -1258,8 +1272,10 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
         }
     } else {
         const int nq = qs.n;
+        int img_l, qi;
+        split_slot(slot, nq, img_l, qi);
         Out* __restrict__ o =
-            reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, slot % nq))) + (size_t)(img0 + slot / nq) * out.img_stride;
+            reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
         const int nc = tile.store_cnt;
         if (out.layout == 0) {
             // the stores of a tile are consecutive slopes: each warp writes rows
