@@ -33,7 +33,6 @@ namespace {
 constexpr int kThreads = 512;
 
 // ---------------------------------------------------------------- helpers
-__device__ __forceinline__ int wrap_once(int j, int H) { return j >= H ? j - H : j; }
 
 __device__ __forceinline__ int wrap_any(int j, int H) {
     if (j >= H) j -= H;
