@@ -701,12 +701,14 @@ __device__ __forceinline__ void by_rows(Acc* __restrict__ d, const Acc* __restri
 
 // Levels 3-5, rows interleaved over lanes (lane l owns rows l, l+32, ...):
 // any shift is one conflict-free wavefront per 32 rows (n <= 256 + 31).
-template <class Acc, int L, int F = 0>
+template <class Acc, int L, int F = 0, int SF = 0>
 __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
     constexpr int w = 1 << L, w0 = w >> 1;
     constexpr int src = ((7 - L + F) & 1) * kBYW, dst = ((6 - L + F) & 1) * kBYW;
     constexpr int G = (kBYMaxS + kBYW + 31) / 32;  // 9 row groups at most
-    const int n = S + kBYW - w;
+    // SF: the row tile known at compile time (the full 256-row tiles): the
+    // row-group predicates of all but the last group fold away
+    const int n = (SF ? SF : S) + kBYW - w;
     const uint32_t base = smem_u32(sm) + lane * 4u;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
@@ -730,12 +732,19 @@ __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
     }
 }
 
+// Levels 3, 4 (shared memory, rows interleaved over lanes) and 5 (stored
+// from registers); full 256-row tiles take the compile-time row count.
+template <class Acc>
+__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+                                              int rows_out);
+
 // Level 5 (the block root) written straight to the pass-0 buffer from
 // registers: lane = row, so each warp store is 32 consecutive rows of one
 // column (coalesced), and the root never round-trips through shared memory.
-template <class Acc>
+template <class Acc, int SF = 0>
 __device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
-                                                int rows_out) {
+                                                int rows_out_) {
+    const int rows_out = SF ? SF : rows_out_;  // SF: a full tile, rows known at compile time
     constexpr int w = 32, w0 = 16;
     constexpr int src = 0;  // level 4 output (parity of V3): slots [0, 32)
     constexpr int G = (kBYMaxS + 31) / 32;
@@ -759,6 +768,25 @@ __device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int la
         for (int u = 0; u < G; ++u)
             if (32 * u + lane < rows_out) g[32 * u] = from_bits<Acc>(add_bits<Acc>(x[u], y[u]));
     }
+}
+
+template <class Acc>
+__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+                                              int rows_out) {
+    if (S == kBYMaxS) {
+        by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 4, 0, kBYMaxS>(sm, S, warp, lane);  // -> slots [0, 32)
+    } else {
+        by_level_s<Acc, 3>(sm, S, warp, lane);
+        __syncthreads();
+        by_level_s<Acc, 4>(sm, S, warp, lane);
+    }
+    __syncthreads();
+    if (rows_out == kBYMaxS)  // a full tile (the last row tile may be shorter)
+        by_level5_store<Acc, kBYMaxS>(sm, S, warp, lane, dcol0, ld, rows_out);
+    else
+        by_level5_store<Acc>(sm, S, warp, lane, dcol0, ld, rows_out);
 }
 
 template <class Acc, int L, int F = 0>
@@ -907,12 +935,8 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
             stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
         by_level12_staged<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
         __syncthreads();
-        by_level_s<Acc, 3>(sm, S, warp, lane);
-        __syncthreads();
-        by_level_s<Acc, 4>(sm, S, warp, lane);  // -> slots [0, 32)
-        __syncthreads();
-        by_level5_store<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
-                             min(S, H - s0));
+        by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+                           min(S, H - s0));
         return;
     }
     if (stage != nullptr) {
@@ -1009,12 +1033,8 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     if constexpr (V >= 4) {  // (V = 5 without staging lands here)
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
-        by_level_s<Acc, 3>(sm, S, warp, lane);
-        __syncthreads();
-        by_level_s<Acc, 4>(sm, S, warp, lane);  // -> slots [0, 32)
-        __syncthreads();
-        by_level5_store<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
-                             min(S, H - s0));
+        by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+                           min(S, H - s0));
         return;
     } else if constexpr (V == 3) {
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
