@@ -292,6 +292,30 @@ __device__ __forceinline__ void rows_op_terms_global(Acc* __restrict__ g, const 
         }
 }
 
+// rows_op_terms for 256 <= n < 288 (a full 256-row tile plus a halo of < 32
+// rows): 8 whole groups with compile-time offsets, then one lane-predicated
+// group -- no loop control.
+template <class Acc, int K, int SPLIT>
+__device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t)[4], int n, int lane) {
+    const uint32_t lo = lane * 4u;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        int v[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 512u * half + 128u * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sts1u(d + lo + 512u * half + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
+    }
+    if (256 + lane < n) {
+        int v[4];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + lo + 1024u);
+        sts1u(d + lo + 1024u, sum_terms<Acc, K, SPLIT>(v));
+    }
+}
+
 template <class Acc, int NWARPS, bool DIRECT>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
@@ -313,7 +337,8 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
             continue;
         }
         if (nt == 4) {
-            rows_op_terms<Acc, 4, 2>(d, t, n, lane);
+            if (n >= 256 && n < 288) rows_op_terms_256<Acc, 4, 2>(d, t, n, lane);
+            else rows_op_terms<Acc, 4, 2>(d, t, n, lane);
         } else if (nt == 2) {
             rows_op_terms<Acc, 2, 1>(d, t, n, lane);
         } else if (nt == 3) {
