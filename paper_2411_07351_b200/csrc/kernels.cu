@@ -316,6 +316,23 @@ __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t
     }
 }
 
+// rows_op_terms_global for exactly 256 rows (a full tile): no loop control
+template <class Acc, int K, int SPLIT>
+__device__ __forceinline__ void rows_op_terms_global_256(Acc* __restrict__ g, const uint32_t (&t)[4], int lane) {
+    const uint32_t lo = lane * 4u;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        int v[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 512u * half + 128u * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            g[128 * half + 32 * u + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v[u]));
+    }
+}
+
 template <class Acc, int NWARPS, bool DIRECT>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
@@ -328,7 +345,9 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
         const int n = h.y, nt = h.z & 7, gc = (h.z >> 3) - 1;
         if (DIRECT && gdst != nullptr && gc >= 0) {  // a stored column (non-root band): straight to the workspace
             Acc* __restrict__ g = gdst + (size_t)gc * ld;
-            if (nt == 4) rows_op_terms_global<Acc, 4, 2>(g, t, rows_out, lane);
+            if (nt == 4 && rows_out == 256) rows_op_terms_global_256<Acc, 4, 2>(g, t, lane);
+            else if (nt == 4) rows_op_terms_global<Acc, 4, 2>(g, t, rows_out, lane);
+            else if (nt == 2 && rows_out == 256) rows_op_terms_global_256<Acc, 2, 1>(g, t, lane);
             else if (nt == 2) rows_op_terms_global<Acc, 2, 1>(g, t, rows_out, lane);
             else if (nt == 3 && q.w == 2) rows_op_terms_global<Acc, 3, 2>(g, t, rows_out, lane);
             else if (nt == 3) rows_op_terms_global<Acc, 3, 1>(g, t, rows_out, lane);
@@ -340,7 +359,8 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
             if (n >= 256 && n < 288) rows_op_terms_256<Acc, 4, 2>(d, t, n, lane);
             else rows_op_terms<Acc, 4, 2>(d, t, n, lane);
         } else if (nt == 2) {
-            rows_op_terms<Acc, 2, 1>(d, t, n, lane);
+            if (n >= 256 && n < 288) rows_op_terms_256<Acc, 2, 1>(d, t, n, lane);
+            else rows_op_terms<Acc, 2, 1>(d, t, n, lane);
         } else if (nt == 3) {
             if (q.w == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
             else rows_op_terms<Acc, 3, 1>(d, t, n, lane);
