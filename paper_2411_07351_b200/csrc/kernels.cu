@@ -431,7 +431,13 @@ __device__ __forceinline__ void run_step_baked(uint32_t base, const int4* __rest
         }
         const uint32_t bb = base + static_cast<uint32_t>(op.z & ~15);
         if (SC) {
-            rows_op_s<Acc>(d, a, bb + 4u * static_cast<uint32_t>(op.z & 3), n, lane);
+            const uint32_t b = bb + 4u * static_cast<uint32_t>(op.z & 3);
+            if (n >= 256 && n < 288) {  // a full tile plus a short halo: fixed shape
+                const uint32_t t[4] = {a, b, 0u, 0u};
+                rows_op_terms_256<Acc, 2, 1>(d, t, n, lane);
+            } else {
+                rows_op_s<Acc>(d, a, b, n, lane);
+            }
             continue;
         }
         switch (op.z & 3) {
