@@ -103,6 +103,7 @@ struct Group {
     // column pitch, offsets of the T / P column sets (-1: not staged)
     long long stage_img = 0, stage_pitch = 0, stage_t = -1, stage_p = -1;
     std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
+    int pm_D = 0;  // u16 pair mode (0: off): workspace words pair rows j and j + pm_D
     size_t slot_bytes = 0;
 };
 
@@ -279,7 +280,10 @@ void upload(Group& g) {
         o.steps = put(pr.step_offs.data(), pr.step_offs.size() * sizeof(int));
         o.ops = put(ps.ops.data(), ps.ops.size() * sizeof(fhtb::PassOp));
         std::vector<int2> stores;
-        for (const auto& st : pr.stores) stores.push_back(make_int2(st.slot, st.gcol));
+        for (const auto& st : pr.stores) {  // u16 pair mode: the root's upper-row slot in bits 16..
+            if (st.slot >= (1 << 16) || st.slot_hi >= (1 << 15)) throw FhtError(FHT_ERR_INTERNAL, "slot index overflow");
+            stores.push_back(make_int2(st.slot | (st.slot_hi >= 0 ? st.slot_hi << 16 : 0), st.gcol));
+        }
         o.stores = put(stores.data(), stores.size() * sizeof(int2));
         // ops baked into shared byte offsets for the 4-byte kernel path
         {
@@ -309,7 +313,11 @@ void upload(Group& g) {
                     if (gcol_of[oi] >= (1 << 27)) throw FhtError(FHT_ERR_INTERNAL, "column index overflow");
                     bops.push_back(make_int4(static_cast<int>(d), static_cast<int>(S + op.ext),
                                              op.nterms | ((gcol_of[oi] + 1) << 3), static_cast<int>(t[0])));
-                    bops.push_back(make_int4(static_cast<int>(t[1]), static_cast<int>(t[2]), static_cast<int>(t[3]), op.split));
+                    // u16 pair mode root ops: the upper-row slot's byte offset above the split
+                    const int64_t dh = op.dst_hi >= 0 ? op.dst_hi * L * 4 : 0;
+                    if (dh >= (int64_t(1) << 27)) throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
+                    bops.push_back(make_int4(static_cast<int>(t[1]), static_cast<int>(t[2]), static_cast<int>(t[3]),
+                                             op.split | static_cast<int>(dh << 4)));
                 }
             }
             for (const auto& op : ps.ops) {
@@ -421,8 +429,21 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const int levels = env_int("FHT_PASS_LEVELS", 5, 1, 8);
         int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
         g->pairs = acc_sz == 4 && env_int("FHT_K2_PAIRS", 1, 0, 1) == 1;
+        // u16 pair mode: u8 images whose root children are at
+        // most 257 wide (every non-root node sum < 2^16) and H <= 512 (one
+        // K1P/K2 row tile of D = H/2 rounded up to 8 words).  It needs the
+        // staged K1P (variant 5) and a single K2 band; FHT_U16_PAIRS=0 turns it off.
+        const int pmD = round_up((H + 1) / 2, 8);
+        bool pm = false;
+        {
+            const auto wc = fhtb::split_width(std::max(W, 2), strategy);
+            const int stage_env0 = env_int("FHT_K1_STAGE", -1, -1, 1);
+            pm = in == FHT_U8 && acc == FHT_I32 && g->pairs && env_int("FHT_U16_PAIRS", 1, 0, 1) == 1 &&
+                 env_int("FHT_K1_BY32", 1, 0, 1) == 1 && env_int("FHT_K1P_VARIANT", 5, 0, 5) == 5 && stage_env0 != 0 &&
+                 bw == 32 && W > 2 * bw && H >= 64 && pmD <= 256 && pmD <= H && std::max(wc.first, wc.second) <= 257;
+        }
         for (;;) {
-            g->sp = SubPlan::build(W, H, strategy, bw, levels, tw);
+            g->sp = SubPlan::build(W, H, strategy, bw, levels, tw, pm);
             bool ok = true;
             for (const auto& ps : g->sp.passes) {
                 const PassProgram pr = program(ps, g->pairs);
@@ -431,10 +452,20 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
                 ok = ok && rows >= std::min(H, 32) &&
                      fhtb::k2_smem_bytes(acc, pr.max_slots, Lmax, pr.max_tile_ops()) <= 227 * 1024;
             }
+            if (pm) {  // one K2 band, row tiles of >= 64 words (or all D)
+                const auto& ps = g->sp.passes;
+                const bool fit = ps.size() == 1 && pass_rows(ps[0], program(ps[0], g->pairs).max_slots, H, acc_sz,
+                                                             budget) >= std::min(pmD, 64);
+                if (!fit) {
+                    pm = false;
+                    continue;  // rebuild without the root's upper-row slots
+                }
+            }
             if (ok) break;
             if (tw == 1) throw FhtError(FHT_ERR_INTERNAL, "fused pass does not fit shared memory");
             tw = std::max(1, tw / 2);
         }
+        g->pm_D = pm ? pmD : 0;
         g->qs.n = static_cast<int>(codes.size());
         for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
         g->ld = round_up(H, acc_sz == 8 ? 16 : 32);
@@ -445,6 +476,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const int ntile = (H + smax - 1) / smax;
         int S = ((H + ntile - 1) / ntile + 7) & ~7;
         if (H < S) S = H;
+        if (pm) S = pmD;  // one tile of D words (rows [0, 2D))
         g->S = S;
         // K1 column stride: 16-byte aligned, vector-merge slack, and room for
         // the row-major staging tile of the horizontal loader (R x (wb+1)).
@@ -460,13 +492,15 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         // staging pays off once the batch is large (its launch costs a few
         // microseconds: a loss for one small image); FHT_K1_STAGE=0/1 forces it
         const int stage_env = env_int("FHT_K1_STAGE", -1, -1, 1);
-        const bool stage_on = stage_env < 0 ? static_cast<int64_t>(batch) * w * h >= (int64_t(8) << 20) : stage_env == 1;
+        const bool stage_on =
+            pm || (stage_env < 0 ? static_cast<int64_t>(batch) * w * h >= (int64_t(8) << 20) : stage_env == 1);
         if (in == FHT_U8 && g->use_by32 && stage_on) {
             // columns of ntile * S + 31 rows (+ the last 4-byte word), 16-byte aligned
             bool need_t = false, need_p = false;
             for (int k = 0; k < g->qs.n; ++k) (codes[static_cast<size_t>(k)] < 2 ? need_t : need_p) = true;
             const long long ntile = (H + S - 1) / S;
-            g->stage_pitch = (ntile * S + 36 + 15) / 16 * 16;
+            // pair mode: rows [0, 2D + 31) (the upper half of every word is D rows on)
+            g->stage_pitch = ((pm ? 2LL * pmD : ntile * S) + 36 + 15) / 16 * 16;
             const long long set = static_cast<long long>(W) * g->stage_pitch;
             g->stage_t = need_t ? 0 : -1;
             g->stage_p = need_p ? (need_t ? set : 0) : -1;
@@ -476,10 +510,15 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         for (size_t i = 0; i < g->sp.passes.size(); ++i) {
             int S2 = std::min(env_int("FHT_K2_SMAX", 256, 32, 4096),
                               pass_rows(g->sp.passes[i], program(g->sp.passes[i], g->pairs).max_slots, H, acc_sz, budget));
-            {  // balance the row tiles
+            if (!pm) {  // balance the row tiles
                 const int nt = (H + S2 - 1) / std::max(1, S2);
                 S2 = std::min(S2, ((H + nt - 1) / nt + 7) & ~7);
                 if (S2 > H) S2 = H;
+            }
+            if (pm) {  // row tiles over the D words, balanced
+                S2 = std::min(S2, pmD);
+                const int nt = (pmD + S2 - 1) / S2;
+                S2 = ((pmD + nt - 1) / nt + 7) & ~7;
             }
             // slot capacity: window + vector-merge slack, a multiple of 4 rows
             // (16-byte aligned slots) with L/4 odd (spreads the transposed
@@ -497,7 +536,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
-        if (g->nby > 0) p->stage_bytes_img = std::max(p->stage_bytes_img, static_cast<size_t>(g->stage_img));
+        if (g->nby > 0 || g->pm_D) p->stage_bytes_img = std::max(p->stage_bytes_img, static_cast<size_t>(g->stage_img));
         max_nq = std::max(max_nq, g->qs.n);
         p->additions += g->sp.additions * static_cast<uint64_t>(g->qs.n) * static_cast<uint64_t>(batch);
         p->groups.push_back(std::move(g));
@@ -516,7 +555,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
     const int nchunks = (batch + chunk - 1) / chunk;
     int per_chunk = 0;
     for (auto& g : p->groups)
-        per_chunk += (g->nblocks > 0 ? 1 : 0) + (g->nby > 0 ? 1 + (g->stage_img > 0 ? 1 : 0) : 0) +
+        per_chunk += (g->nblocks > 0 ? 1 : 0) + (g->nby > 0 ? 1 : 0) + ((g->nby > 0 || g->pm_D) && g->stage_img > 0 ? 1 : 0) +
                      static_cast<int>(g->sp.passes.size());
     p->launches = per_chunk * nchunks;
     return p.release();
@@ -561,7 +600,8 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.blocks = g.dt.blocks;
             L.nby = g.nby;
             L.by_x0 = g.dt.by_x0;
-            L.k1p_variant = env_int("FHT_K1P_VARIANT", 5, 0, 5);  // see GroupLaunch
+            L.k1p_variant = g.pm_D ? 5 : env_int("FHT_K1P_VARIANT", 5, 0, 5);  // see GroupLaunch
+            L.pm_D = g.pm_D;
             L.k2_scalar = env_int("FHT_K2_SCALAR", 1, 0, 1);
             L.k2_bulk = env_int("FHT_K2_BULK", 0, 0, 1);
             L.pdl = env_int("FHT_PDL", 1, 0, 1);
@@ -773,7 +813,7 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
             for (int k = 0; k < g.qs.n; ++k) o << (k ? "," : "") << g.qs.code[k];
             o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"nbuf\":" << g.nbuf
               << ",\"level_pairs\":" << (g.pairs ? "true" : "false") << ",\"stage_pitch\":" << g.stage_pitch
-              << ",\"stage_bytes\":" << g.stage_img << ",\"pass_rows\":[";
+              << ",\"stage_bytes\":" << g.stage_img << ",\"u16_pair_D\":" << g.pm_D << ",\"pass_rows\":[";
             for (size_t k = 0; k < g.dt.passes.size(); ++k)
                 o << (k ? "," : "") << "[" << g.dt.passes[k].S << "," << g.dt.passes[k].L << "]";
             o << "],\"plan\":" << g.sp.describe() << "}";

@@ -203,6 +203,23 @@ __device__ __forceinline__ int add_bits(int x, int y) {
     return to_bits<Acc>(from_bits<Acc>(x) + from_bits<Acc>(y));
 }
 
+// u16 pair mode: a 32-bit word j of a working column holds
+// rows j (low half) and j + D (high half), both < 2^16 (a node of width w
+// sums w u8 leaves: w * 255 < 2^16 for every node below the root when the
+// root's children are at most 257 wide).  One integer add then advances
+// both rows, and the shifts of the DP -- the same for every row -- act on
+// whole words.  pack_pair_u8x4: 4 staged leaf rows of each half -> 4 words.
+__device__ __forceinline__ int4 pack_pair_u8x4(uint32_t lo, uint32_t hi) {
+    const uint32_t t0 = __byte_perm(lo, hi, 0x5410), t1 = __byte_perm(lo, hi, 0x7632);  // lo0 lo1 hi0 hi1 | ..
+    return make_int4(static_cast<int>(__byte_perm(t0, 0u, 0x4240)), static_cast<int>(__byte_perm(t0, 0u, 0x4341)),
+                     static_cast<int>(__byte_perm(t1, 0u, 0x4240)), static_cast<int>(__byte_perm(t1, 0u, 0x4341)));
+}
+
+// Word j of the pair layout for j in [D, H): rows j and (j + D) mod H =
+// j - D + e (e = 2D - H), i.e. the high half of word j - D and the low half
+// of word j - D + e.  The tile computes words [0, D) only (every row once).
+__device__ __forceinline__ int pair_extra_word(int w_k, int w_ke) { return static_cast<int>(__byte_perm(w_k, w_ke, 0x5432)); }
+
 // The same op with rows interleaved over lanes (lane l owns rows l, l+32,
 // ...): 32 consecutive words are conflict-free at any alignment, so the
 // shifted operand costs one wavefront per 32 rows like the aligned ones
@@ -333,6 +350,59 @@ __device__ __forceinline__ void rows_op_terms_global_256(Acc* __restrict__ g, co
     }
 }
 
+// The root step of the u16 pair mode: the children's sums x (first child)
+// and y (second child) are packed words (each half < 2^16); the root adds
+// them half by half into two 32-bit columns -- rows [0, S) of the tile to d,
+// rows [D, D + S) to dh.  Same add order as the tree (x + y per row).
+template <int K, int SPLIT>
+__device__ __forceinline__ void child_sums(const int (&v)[4], uint32_t& x, uint32_t& y) {
+    const uint32_t a = static_cast<uint32_t>(v[0]), b = static_cast<uint32_t>(v[1]), c = static_cast<uint32_t>(v[2]),
+                   d = static_cast<uint32_t>(v[3]);
+    if constexpr (K == 1) x = a, y = 0u;
+    else if constexpr (K == 2) x = a, y = b;
+    else if constexpr (K == 3 && SPLIT == 2) x = a + b, y = c;
+    else if constexpr (K == 3) x = a, y = b + c;
+    else x = a + b, y = c + d;
+}
+template <int K, int SPLIT>
+__device__ __forceinline__ void rows_op_widen(uint32_t d, uint32_t dh, const uint32_t (&t)[4], int n, int lane) {
+    constexpr int U = 2;
+    const uint32_t lo = lane * 4u;
+    for (int i0 = 0; i0 < n; i0 += 32 * U) {
+        int v[U][4];
+        const uint32_t o = lo + i0 * 4u;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + 32 * u + lane < n)
+#pragma unroll
+                for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + 32 * u + lane < n) {
+                uint32_t x, y;
+                child_sums<K, SPLIT>(v[u], x, y);
+                sts1u(d + o + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
+                sts1u(dh + o + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
+            }
+    }
+}
+template <int NWARPS>
+__device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
+                                               int warp, int lane) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 h = ops[2 * o], q = ops[2 * o + 1];
+        const uint32_t d = base + static_cast<uint32_t>(h.x), dh = base + (static_cast<uint32_t>(q.w) >> 4);
+        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        const int n = h.y, nt = h.z & 7, split = q.w & 15;
+        if (nt == 4) rows_op_widen<4, 2>(d, dh, t, n, lane);
+        else if (nt == 2) rows_op_widen<2, 1>(d, dh, t, n, lane);
+        else if (nt == 3 && split == 2) rows_op_widen<3, 2>(d, dh, t, n, lane);
+        else if (nt == 3) rows_op_widen<3, 1>(d, dh, t, n, lane);
+        else rows_op_widen<1, 1>(d, dh, t, n, lane);
+    }
+}
+
 template <class Acc, int NWARPS, bool DIRECT>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
@@ -349,7 +419,7 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
             else if (nt == 4) rows_op_terms_global<Acc, 4, 2>(g, t, rows_out, lane);
             else if (nt == 2 && rows_out == 256) rows_op_terms_global_256<Acc, 2, 1>(g, t, lane);
             else if (nt == 2) rows_op_terms_global<Acc, 2, 1>(g, t, rows_out, lane);
-            else if (nt == 3 && q.w == 2) rows_op_terms_global<Acc, 3, 2>(g, t, rows_out, lane);
+            else if (nt == 3 && (q.w & 15) == 2) rows_op_terms_global<Acc, 3, 2>(g, t, rows_out, lane);
             else if (nt == 3) rows_op_terms_global<Acc, 3, 1>(g, t, rows_out, lane);
             else
                 for (int i = lane; i < rows_out; i += 32) g[i] = from_bits<Acc>(lds1u(t[0] + 4u * i));
@@ -362,7 +432,7 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
             if (n >= 256 && n < 288) rows_op_terms_256<Acc, 2, 1>(d, t, n, lane);
             else rows_op_terms<Acc, 2, 1>(d, t, n, lane);
         } else if (nt == 3) {
-            if (q.w == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
+            if ((q.w & 15) == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
             else rows_op_terms<Acc, 3, 1>(d, t, n, lane);
         } else {  // a single term: copy
             for (int i = lane; i < n; i += 32) sts1u(d + 4u * i, lds1u(t[0] + 4u * i));
@@ -501,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, const int4* __restrict__ bops, int max_width,
     int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
-    long long spitch, long long simg, long long st_t, long long st_p) {
+    long long spitch, long long simg, long long st_t, long long st_p, int pmD) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
@@ -535,6 +605,11 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
         for (int c = warp; c < wb; c += kWarps) {
             const int col = (q & 1) ? W - 1 - (x0 + c) : x0 + c;
             const uint32_t* __restrict__ cp = reinterpret_cast<const uint32_t*>(sb + (size_t)col * spitch);
+            if (pmD) {  // u16 pair mode: words of rows (i, i + D)
+                for (int k = lane; k < nw; k += 32)
+                    sts4(lbuf + c * sr + 4 * k, pack_pair_u8x4(__ldg(cp + k), __ldg(cp + k + (pmD >> 2))));
+                continue;
+            }
             for (int k = lane; k < nw; k += 32) {
                 const uint32_t x = __ldg(cp + k);
                 sts4(lbuf + c * sr + 4 * k,
@@ -605,6 +680,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
         const bool al = ((ld | s0) & 3) == 0;
         for (int c = warp; c < wb; c += kWarps)
             warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, buf0 + c * sr, rows_out, al, lane);
+        if (pmD) {  // u16 pair mode: words [D, H) from words k and k + e of the root
+            const int e = 2 * pmD - H;
+            for (int c = warp; c < wb; c += kWarps) {
+                const Acc* rc = buf0 + c * sr;
+                Acc* __restrict__ gc = dstw + (size_t)(x0 + c) * ld + pmD;
+                for (int k = lane; k < H - pmD; k += 32)
+                    gc[k] = from_bits<Acc>(pair_extra_word(to_bits<Acc>(rc[k]), to_bits<Acc>(rc[k + e])));
+            }
+        }
     } else {
         Out* o = reinterpret_cast<Out*>(out_ptr(out, q)) + (size_t)img_i * out.img_stride;
         if (out.layout == 0) {  // rows of wb contiguous slopes
@@ -956,6 +1040,84 @@ __device__ __forceinline__ void by_level12_staged(Acc* sm, int S, int tid, const
     }
 }
 
+// by_level12_staged in the u16 pair mode: the leaf words pack rows 4j.. of
+// the low half with rows 4j + D.. of the high half (both aligned: D % 4 == 0).
+template <class Acc>
+__device__ __forceinline__ void by_level12_staged_pair(Acc* sm, int S, int tid, const unsigned char* __restrict__ sb,
+                                                       long long spitch, int W, int x0, bool rev, int D) {
+    const int nchunk = (S + kBYW - 4 + 3) >> 2;
+    int4* O = reinterpret_cast<int4*>(sm);
+    constexpr int s4 = kBYSR / 4;
+    const int g = tid >> 6;
+    const int dw = D >> 2;  // the high half, in 4-byte words
+    for (int j = tid & 63; j < nchunk; j += 64) {
+        const int c = x0 + 4 * g;
+        const long long cs = rev ? -spitch : spitch;
+        const unsigned char* pa = sb + (long long)(rev ? W - 1 - c : c) * spitch + 4 * j;
+        const uint32_t* A = reinterpret_cast<const uint32_t*>(pa);
+        const uint32_t* B = reinterpret_cast<const uint32_t*>(pa + cs);
+        const uint32_t* E = reinterpret_cast<const uint32_t*>(pa + 2 * cs);
+        const uint32_t* F = reinterpret_cast<const uint32_t*>(pa + 3 * cs);
+        const uint32_t wa0 = __ldg(A), wb0 = __ldg(B), wb1 = __ldg(B + 1), we0 = __ldg(E), we1 = __ldg(E + 1),
+                       wf0 = __ldg(F), wf1 = __ldg(F + 1);
+        const uint32_t ha0 = __ldg(A + dw), hb0 = __ldg(B + dw), hb1 = __ldg(B + dw + 1), he0 = __ldg(E + dw),
+                       he1 = __ldg(E + dw + 1), hf0 = __ldg(F + dw), hf1 = __ldg(F + dw + 1);
+        const int4 a0 = pack_pair_u8x4(wa0, ha0), b0 = pack_pair_u8x4(wb0, hb0), b1 = pack_pair_u8x4(wb1, hb1);
+        const int4 e0 = pack_pair_u8x4(we0, he0), e1 = pack_pair_u8x4(we1, he1), f0 = pack_pair_u8x4(wf0, hf0),
+                   f1 = pack_pair_u8x4(wf1, hf1);
+        const int4 p0l = add4<Acc>(a0, b0);
+        const int4 p1l = add4<Acc>(a0, shifted<1>(b0, b1));
+        const int4 q0l = add4<Acc>(e0, f0), q0h = add4<Acc>(e1, f1);
+        const int4 q1l = add4<Acc>(e0, shifted<1>(f0, f1)), q1h = add4<Acc>(e1, shifted<1>(f1, f1));
+        const int d0 = (4 * g) * s4 + j;
+        O[d0] = add4<Acc>(p0l, q0l);
+        O[d0 + s4] = add4<Acc>(p0l, shifted<1>(q0l, q0h));
+        O[d0 + 2 * s4] = add4<Acc>(p1l, shifted<1>(q1l, q1h));
+        O[d0 + 3 * s4] = add4<Acc>(p1l, shifted<2>(q1l, q1h));
+    }
+}
+
+// Level 5 of the pair mode: words [0, D) stored from registers as in
+// by_level5_store, then words [D, H) formed with two shuffles per group.
+template <class Acc>
+__device__ __forceinline__ void by_level5_store_pair(Acc* sm, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+                                                     int D, int H) {
+    constexpr int w = 32, w0 = 16;
+    constexpr int G = kBYMaxS / 32;  // D <= 256
+    const int e = 2 * D - H, nx = H - D;
+    const int sl = (lane + e) & 31;
+    const bool same = lane + e < 32;
+    const uint32_t base = smem_u32(sm) + lane * 4u;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        const int T = warp + h * kWarpsBY;
+        const int t0 = (2 * T * (w0 - 1) + (w - 1)) / (2 * (w - 1));
+        const int r = T - t0;
+        const uint32_t a = base + t0 * kBYSR * 4u;
+        const uint32_t b = base + ((w0 + t0) * kBYSR + r) * 4u;
+        Acc* __restrict__ g = dcol0 + (size_t)T * ld + lane;
+        int x[G], y[G], v[G + 1];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            if (32 * u + lane < D) {
+                x[u] = lds1u(a + 128u * u);
+                y[u] = lds1u(b + 128u * u);
+            }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            v[u] = 32 * u + lane < D ? add_bits<Acc>(x[u], y[u]) : 0;
+            if (32 * u + lane < D) g[32 * u] = from_bits<Acc>(v[u]);
+        }
+        v[G] = 0;
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            if (32 * u >= nx) break;  // warp-uniform
+            const int s0v = __shfl_sync(0xffffffffu, v[u], sl), s1v = __shfl_sync(0xffffffffu, v[u + 1], sl);
+            if (32 * u + lane < nx) g[D + 32 * u] = from_bits<Acc>(pair_extra_word(v[u], same ? s0v : s1v));
+        }
+    }
+}
+
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
 template <class In, class Acc, int V>
 __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
@@ -963,7 +1125,7 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
                                                           int ld, int S, const int* __restrict__ bx0,
                                                           Acc* __restrict__ ws, int nbuf,
                                                           const unsigned char* __restrict__ stage, long long spitch,
-                                                          long long simg, long long st_t, long long st_p) {
+                                                          long long simg, long long st_t, long long st_p, int pmD) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
@@ -984,6 +1146,22 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
         // levels 1-2 read the staged columns directly (no leaf tile)
         const unsigned char* __restrict__ sb =
             stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
+        if (pmD) {  // u16 pair mode: one tile of words [0, D), S == D
+            by_level12_staged_pair<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0, pmD);
+            __syncthreads();
+            if (S == kBYMaxS) {
+                by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
+                __syncthreads();
+                by_level_s<Acc, 4, 0, kBYMaxS>(sm, S, warp, lane);
+            } else {
+                by_level_s<Acc, 3>(sm, S, warp, lane);
+                __syncthreads();
+                by_level_s<Acc, 4>(sm, S, warp, lane);
+            }
+            __syncthreads();
+            by_level5_store_pair<Acc>(sm, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld, ld, pmD, H);
+            return;
+        }
         by_level12_staged<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
         __syncthreads();
         by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
@@ -1251,10 +1429,48 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
 // MODE 0: one level per step, 4 rows per lane; 1: rows interleaved over
 // lanes; 2: level-pair programs (4-byte accumulators only); 4: level pairs of
 // a non-root band, its last step storing the band's columns from registers.
+// Root store, reference layout, 4-byte accumulators: rows [0, rows) of the
+// tile's columns (slots at sa0 for lanes < 32, sa1 for 32..63) to output
+// rows r0.. of slopes t0 + lane; lane = slope, 16-byte shared reads of 4
+// rows, 4 coalesced row stores; one row pointer per warp advanced by a fixed
+// stride (the 64-bit address math per store dominated otherwise).
+template <class Acc, class Out, int NWARPS>
+__device__ __forceinline__ void store_root_rows(Out* __restrict__ o, int W, int t0, int nc, uint32_t sa0,
+                                                uint32_t sa1, int r0, int rows, int warp, int lane) {
+    const size_t wstep = (size_t)W * (NWARPS * 4);
+    Out* __restrict__ prow = o + (size_t)(r0 + warp * 4) * W + t0 + lane;
+    int i = warp * 4;
+    for (; i + 4 <= rows; i += NWARPS * 4, prow += wstep) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (lane + 32 * h >= nc) continue;
+            const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
+            Out* __restrict__ p = prow + 32 * h;
+            p[0] = static_cast<Out>(from_bits<Acc>(v4.x));
+            p[W] = static_cast<Out>(from_bits<Acc>(v4.y));
+            p[2 * W] = static_cast<Out>(from_bits<Acc>(v4.z));
+            p[3 * W] = static_cast<Out>(from_bits<Acc>(v4.w));
+        }
+    }
+    if (i < rows) {  // the last 1-3 rows
+        const int nr = rows - i;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (lane + 32 * h >= nc) continue;
+            const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
+            const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < nr) prow[32 * h + (size_t)k * W] = static_cast<Out>(from_bits<Acc>(vv[k]));
+        }
+    }
+}
+
 template <class Acc, class Out, int MODE>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
-                                                     int ld, bool final_pass, OutDesc out, QuadSet qs, int img0) {
+                                                     int ld, bool final_pass, OutDesc out, QuadSet qs, int img0,
+                                                     int pmD) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
@@ -1272,7 +1488,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     int* ssteps = reinterpret_cast<int*>(sops + ps.max_tile_ops);  // the tile's step offsets (after the ops)
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid];
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
-    if constexpr (MODE == 2 || MODE == 4) {
+    if constexpr (MODE == 2 || MODE == 4 || MODE == 6) {
         for (int k = tid; k < 2 * nops; k += kThreads2) sbops[k] = ps.bops[2 * op0 + k];
     } else if constexpr (sizeof(Acc) == 4) {
         for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
@@ -1312,6 +1528,10 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
         if constexpr (MODE == 2) {
             run_step_terms<Acc, kWarps, false>(sbase, sbops, ob, oe, warp, lane);
+        } else if constexpr (MODE == 6) {
+            // u16 pair mode: the root step widens the packed halves to 32 bits
+            if (k + 1 < tile.nsteps) run_step_terms<Acc, kWarps, false>(sbase, sbops, ob, oe, warp, lane);
+            else run_step_widen<kWarps>(sbase, sbops, ob, oe, warp, lane);
         } else if constexpr (MODE == 4) {
             // the last step of a non-root band stores its columns from registers
             const bool direct = k + 1 == tile.nsteps;
@@ -1326,7 +1546,9 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     }
     __syncthreads();
     // 3. store the tile's columns (window offset 0, rows [s0, s0 + S) clipped to H)
-    const int rows = min(S, H - s0);
+    // (u16 pair mode: the tiles cover words [0, D); word j holds rows j and j + D)
+    const int rows = MODE == 6 ? min(S, pmD - s0) : min(S, H - s0);
+    const int rows_hi = MODE == 6 ? max(0, min(rows, H - pmD - s0)) : 0;
     if (MODE == 4 && tile.nsteps > 0) return;  // stored by the last step
     if (!final_pass) {
         Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
@@ -1351,39 +1573,18 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
             // the stores of a tile are consecutive slopes: each warp writes rows
             // of nc (<= 64) contiguous t
             const int t0 = ps.stores[tile.store_beg].y;
-            const int sl0 = lane < nc ? ps.stores[tile.store_beg + lane].x : 0;
-            const int sl1 = lane + 32 < nc ? ps.stores[tile.store_beg + lane + 32].x : 0;
+            const int x0r = lane < nc ? ps.stores[tile.store_beg + lane].x : 0;
+            const int x1r = lane + 32 < nc ? ps.stores[tile.store_beg + lane + 32].x : 0;
+            // u16 pair mode: .x = lo slot | hi slot << 16
+            const int sl0 = MODE == 6 ? (x0r & 0xffff) : x0r, sl1 = MODE == 6 ? (x1r & 0xffff) : x1r;
             if constexpr (sizeof(Acc) == 4) {
-                // lane = slope; 16-byte smem reads of 4 rows, 4 coalesced row
-                // stores; one row pointer per warp advanced by a fixed stride
-                // (the 64-bit address math per store dominated otherwise)
-                const uint32_t sa0 = smem_u32(sm + (size_t)sl0 * L), sa1 = smem_u32(sm + (size_t)sl1 * L);
-                const size_t wstep = (size_t)W * (kWarps * 4);
-                Out* __restrict__ prow = o + (size_t)(s0 + warp * 4) * W + t0 + lane;
-                int i = warp * 4;
-                for (; i + 4 <= rows; i += kWarps * 4, prow += wstep) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (lane + 32 * h >= nc) continue;
-                        const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
-                        Out* __restrict__ p = prow + 32 * h;
-                        p[0] = static_cast<Out>(from_bits<Acc>(v4.x));
-                        p[W] = static_cast<Out>(from_bits<Acc>(v4.y));
-                        p[2 * W] = static_cast<Out>(from_bits<Acc>(v4.z));
-                        p[3 * W] = static_cast<Out>(from_bits<Acc>(v4.w));
-                    }
-                }
-                if (i < rows) {  // the last 1-3 rows
-                    const int nr = rows - i;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (lane + 32 * h >= nc) continue;
-                        const int4 v4 = lds4u((h ? sa1 : sa0) + i * 4u);
-                        const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (k < nr) prow[32 * h + (size_t)k * W] = static_cast<Out>(from_bits<Acc>(vv[k]));
-                    }
+                // u16 pair mode: then the upper rows [D + s0, ...) from the hi slots
+#pragma unroll 1
+                for (int half = 0; half < (MODE == 6 ? 2 : 1); ++half) {
+                    const int a0 = half ? x0r >> 16 : sl0, a1 = half ? x1r >> 16 : sl1;
+                    const int r0 = half ? s0 + pmD : s0, nr = half ? rows_hi : rows;
+                    store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, smem_u32(sm + (size_t)a0 * L),
+                                                      smem_u32(sm + (size_t)a1 * L), r0, nr, warp, lane);
                 }
             } else {
                 for (int i = warp; i < rows; i += kWarps) {
@@ -1394,6 +1595,17 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
             }
         } else {
             Out* __restrict__ pr = static_cast<Out*>(out.peer);
+            if constexpr (MODE == 6) {  // u16 pair mode, slope-major output: both halves
+                for (int c = warp; c < nc; c += kWarps) {
+                    const int2 st = ps.stores[tile.store_beg + c];
+                    const Acc* sv = sm + (size_t)(st.x & 0xffff) * L;
+                    const Acc* sh = sm + (size_t)(st.x >> 16) * L;
+                    Out* __restrict__ dcol = o + (size_t)st.y * H + s0;
+                    for (int i = lane; i < rows; i += 32) dcol[i] = static_cast<Out>(sv[i]);
+                    for (int i = lane; i < rows_hi; i += 32) dcol[pmD + i] = static_cast<Out>(sh[i]);
+                }
+                return;
+            }
             for (int c = warp; c < nc; c += kWarps) {
                 const int2 st = ps.stores[tile.store_beg + c];
                 const Acc* sv = sm + (size_t)st.x * L;
@@ -1497,7 +1709,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     // u8 staging (large batches): the aligned working columns K1 and K1P read
     const unsigned char* stage = nullptr;
     if constexpr (sizeof(Acc) == 4 && std::is_same<In, unsigned char>::value) {
-        if (g.nby > 0 && g.stage != nullptr) {
+        if ((g.nby > 0 || g.pm_D) && g.stage != nullptr) {
             const auto* im = reinterpret_cast<const unsigned char*>(g.img);
             const long long ext_w = std::max<long long>(g.img_w, g.stage_p >= 0 ? g.stage_pitch : 0);
             const long long ext_h = std::max<long long>(g.img_h, g.stage_t >= 0 ? g.stage_pitch : 0);
@@ -1516,13 +1728,13 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         cudaStreamWaitEvent(st1, g.ev_fork, 0);
     }
     if (g.nblocks > 0) {
-        dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
+        dim3 g1(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nblocks, nslots);
         auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;
         allow_smem(reinterpret_cast<const void*>(k1));
         launch_k(g.pdl && !both, k1, g1, dim3(kThreads), smem, st1, reinterpret_cast<const In*>(g.img), g.img_w,
                  g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs,
                  g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out, stage,
-                 g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
+                 g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D);
         ++launches;
         if (hook) hook(ctx, 1);
     }
@@ -1535,10 +1747,10 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                                            : k1_by32<In, Acc, 5>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
             allow_smem(reinterpret_cast<const void*>(kb));
-            dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
+            dim3 gb(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nby, nslots);
             launch_k(g.pdl, kb, gb, dim3(kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w, g.img_h,
                      g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf, stage,
-                     g.stage_pitch, g.stage_img, g.stage_t, g.stage_p);
+                     g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, stage ? g.pm_D : 0);
             ++launches;
             if (hook) hook(ctx, 4);
         }
@@ -1560,13 +1772,16 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             // level pairs; non-root bands (MODE 4) store their columns from registers
             if (ps.pairs) k2 = final_pass ? k2_pass<Acc, Out, 2> : k2_pass<Acc, Out, 4>;
             else if (g.k2_scalar) k2 = k2_pass<Acc, Out, 1>;
+            if constexpr (std::is_same<Acc, int32_t>::value) {
+                if (ps.pairs && final_pass && g.pm_D) k2 = k2_pass<Acc, Out, 6>;  // u16 pair mode root band
+            }
         }
         PassDev pd = ps;
         pd.bulk = g.k2_bulk;
         allow_smem(reinterpret_cast<const void*>(k2));
-        dim3 g2((g.H + ps.S - 1) / ps.S, ps.ntiles, nslots);
+        dim3 g2(((g.pm_D ? g.pm_D : g.H) + ps.S - 1) / ps.S, ps.ntiles, nslots);
         launch_k(g.pdl, k2, g2, dim3(kThreads2), smem2, st, pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out,
-                 g.qs, g.img0);
+                 g.qs, g.img0, g.pm_D);
         ++launches;
         if (hook) hook(ctx, final_pass ? 3 : 2);
     }

@@ -109,6 +109,9 @@ struct GroupLaunch {
     // working columns of the horizontal quadrants (image columns, at
     // stage_t) and/or of the vertical ones (image rows, at stage_p), W
     // columns of stage_pitch bytes each, rows past H wrapped
+    // u16 pair mode (0: off): workspace words hold rows (j, j + pm_D);
+    // K1/K1P/K2 run one row tile of pm_D words, K2's root step widens to 32 bits
+    int pm_D;
     unsigned char* stage;
     long long stage_pitch, stage_img;
     long long stage_t, stage_p;  // byte offsets inside an image's stage (-1: not staged)

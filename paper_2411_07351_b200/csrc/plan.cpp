@@ -313,6 +313,7 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
                 pslot[static_cast<size_t>(n)][static_cast<size_t>(t)] = ent[static_cast<size_t>(n)][static_cast<size_t>(t)].slot;
     int pnext = tile.load_cnt;
     std::vector<int> pfree;
+    std::vector<int> phi(static_cast<size_t>(nodes[static_cast<size_t>(X)].w), -1);  // root upper-row slots
     std::vector<std::pair<int, int>> plive;
     for (int n : order)
         if (front[static_cast<size_t>(n)])
@@ -362,6 +363,15 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
                         pfree.pop_back();
                     }
                     pslot[static_cast<size_t>(n)][static_cast<size_t>(t)] = op.dst;
+                    if (ps.root_hi && X == 0 && n == X) {  // the widened root's upper rows
+                        if (pfree.empty()) {
+                            op.dst_hi = pnext++;
+                        } else {
+                            op.dst_hi = pfree.back();
+                            pfree.pop_back();
+                        }
+                        phi[static_cast<size_t>(t)] = op.dst_hi;
+                    }
                     ps.pops.push_back(op);
                     plive.push_back({n, t});
                 }
@@ -378,7 +388,8 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
         plive.swap(keep);
     }
     ps.pstep_offs.push_back(static_cast<int>(ps.pops.size()));
-    for (int t = ta; t < tb; ++t) ps.pstores.push_back({pslot[static_cast<size_t>(X)][static_cast<size_t>(t)], xn.x0 + t});
+    for (int t = ta; t < tb; ++t)
+        ps.pstores.push_back({pslot[static_cast<size_t>(X)][static_cast<size_t>(t)], xn.x0 + t, phi[static_cast<size_t>(t)]});
     pt.nslots = pnext;
     ps.pmax_slots = std::max(ps.pmax_slots, pnext);
     ps.ptiles.push_back(pt);
@@ -386,7 +397,7 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
 
 }  // namespace
 
-SubPlan SubPlan::build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width) {
+SubPlan SubPlan::build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width, bool root_hi) {
     if (W < 1 || H < 1) throw std::invalid_argument("fht2d: image is empty");
     if (strategy != kSimple && strategy != kTweaked) throw std::invalid_argument("unknown split strategy");
     if (block_width < 1 || block_width > 64) throw std::invalid_argument("block width must lie in [1, 64]");
@@ -445,6 +456,7 @@ SubPlan SubPlan::build(int W, int H, int strategy, int block_width, int pass_lev
         std::vector<char> nfront(nodes.size(), 0);
         FusedPass ps;
         ps.tile_width = tile_width;
+        ps.root_hi = root_hi;
         for (size_t i = 0; i < nodes.size(); ++i) {
             if (below[i]) continue;
             const bool top = (i == 0) || height[static_cast<size_t>(parent[i])] > k;

@@ -77,6 +77,7 @@ struct PassOp {
 };
 struct PassStore {
     int slot, gcol;
+    int slot_hi = -1;  // u16 pair mode: the slot of the root column's upper-half rows
 };
 struct PassTile {
     int load_beg, load_cnt, step_beg, nsteps, store_beg, store_cnt, nslots, max_ext;
@@ -91,6 +92,7 @@ struct PassOpN {
     int dst, ext, nterms;
     PassTerm term[4];
     int split;  // terms [0, split) form the first child: sum = (first) + (rest), the tree's add order
+    int dst_hi = -1;  // u16 pair mode, root ops: the widened upper-half rows go to this slot
 };
 struct FusedPass {
     int levels = 0;  // tree levels this pass advances (max over its tiles)
@@ -109,6 +111,7 @@ struct FusedPass {
     std::vector<PassOpN> pops;
     std::vector<PassStore> pstores;
     int pmax_slots = 0;
+    bool root_hi = false;  // the root ops carry dst_hi (u16 pair mode)
 };
 
 // The schedule for one working orientation (width W = number of slopes,
@@ -124,7 +127,10 @@ struct SubPlan {
     int tree_depth = 0;      // levels of the whole tree (= ceil(log2 W) for Tweaked)
     uint64_t additions = 0;  // count_additions_tree(W, H)
 
-    static SubPlan build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width);
+    // root_hi: the root band's level-pair ops get a second output slot (the
+    // widening root step of the u16 pair mode)
+    static SubPlan build(int W, int H, int strategy, int block_width, int pass_levels, int tile_width,
+                         bool root_hi = false);
     std::string describe() const;
 };
 

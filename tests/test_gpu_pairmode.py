@@ -1,0 +1,93 @@
+"""GPU parity of the u16 pair mode: u8 images whose root
+children are at most 257 wide run with 32-bit words holding rows j and
+j + D, the root step widening to int32.  Bit-exact against the oracle at the
+shape limits, for worst-case (all-255) images, odd and even heights, both
+strategies, int64 output, the native layout and single quadrants; and
+against the mode switched off (FHT_U16_PAIRS=0)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_07351_b200 import fht
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+Q = oracle.QUADRANTS
+
+
+def _run(imgs, strategy=1, quadrants="all", layout="reference", out_dtype=None):
+    b, h, w = imgs.shape
+    plan = fht.Plan(w, h, strategy, in_dtype="u8", acc_dtype="i32", out_dtype=out_dtype, quadrants=quadrants,
+                    batch=b, layout=layout)
+    out = plan(torch.from_numpy(np.ascontiguousarray(imgs)).cuda())
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}, plan.describe()
+
+
+def _pair_d(desc):
+    return [g["u16_pair_D"] for g in desc["groups"]]
+
+
+@pytest.mark.parametrize("h,w,strategy", [(509, 509, 1), (512, 512, 1), (64, 65, 1), (65, 300, 0), (511, 96, 1),
+                                          (120, 258, 0), (130, 257, 1), (333, 77, 0)])
+def test_pair_mode_bit_exact(h, w, strategy):
+    rng = np.random.default_rng(h * 1000 + w)
+    imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)
+    imgs[1] = 255  # the overflow worst case: every node sum at its bound
+    out, desc = _run(imgs, strategy)
+    assert any(d > 0 for d in _pair_d(desc)), desc
+    for bi in range(2):
+        ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} s{strategy} {k} img{bi}")
+
+
+def test_pair_mode_off_beyond_limits():
+    # root children of 514 (Tweaked: 256 + 258) exceed 257: the mode stays off
+    _, desc = _run(np.zeros((1, 100, 514), np.uint8), 1, quadrants="horiz_pos")
+    assert _pair_d(desc) == [0]
+    # H > 512: D would exceed one 256-word tile
+    _, desc = _run(np.zeros((1, 513, 300), np.uint8), 1, quadrants="horiz_pos")
+    assert _pair_d(desc) == [0]
+
+
+def test_pair_mode_layouts_widening_quadrants(monkeypatch):
+    rng = np.random.default_rng(7)
+    imgs = rng.integers(0, 256, (3, 300, 420), dtype=np.uint8)
+    ref = [oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int64)[0] for i in range(3)]
+    out, desc = _run(imgs, 1, out_dtype="i64")
+    assert all(d > 0 for d in _pair_d(desc))
+    for i in range(3):
+        for k in Q:
+            assert out[k].dtype == np.int64
+            np.testing.assert_array_equal(out[k][i], ref[i][k])
+    out, _ = _run(imgs, 1, layout="native")
+    for i in range(3):
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i], ref[i][k].T)
+    for q in ("vert_neg", "horiz_pos"):
+        out, _ = _run(imgs, 1, quadrants=q)
+        for i in range(3):
+            np.testing.assert_array_equal(out[q][i], ref[i][q])
+    # the same bytes with the mode switched off
+    monkeypatch.setenv("FHT_U16_PAIRS", "0")
+    out0, desc0 = _run(imgs, 1)
+    assert _pair_d(desc0) == [0, 0]
+    for i in range(3):
+        for k in Q:
+            np.testing.assert_array_equal(out0[k][i], ref[i][k])
+
+
+def test_pair_mode_host_buffers():
+    rng = np.random.default_rng(3)
+    imgs = rng.integers(0, 256, (5, 509, 509), dtype=np.uint8)
+    plan = fht.Plan(509, 509, 1, in_dtype="u8", acc_dtype="i32", quadrants="all", batch=5)
+    out = plan.execute_host(imgs)
+    for i in (0, 4):
+        ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i], ref[k])
