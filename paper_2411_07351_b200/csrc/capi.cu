@@ -442,6 +442,9 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
                  env_int("FHT_K1_BY32", 1, 0, 1) == 1 && env_int("FHT_K1P_VARIANT", 5, 0, 5) == 5 && stage_env0 != 0 &&
                  bw == 32 && W > 2 * bw && H >= 64 && pmD <= 256 && pmD <= H && std::max(wc.first, wc.second) <= 257;
         }
+        // pair mode: 16-slope tiles (the root's upper-row slots then leave room
+        // for one row tile of all D words at two CTAs per SM; measured faster)
+        if (pm && !std::getenv("FHT_TILE_WIDTH")) tw = 16;
         for (;;) {
             g->sp = SubPlan::build(W, H, strategy, bw, levels, tw, pm);
             bool ok = true;
@@ -458,6 +461,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
                                                              budget) >= std::min(pmD, 64);
                 if (!fit) {
                     pm = false;
+                    tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);
                     continue;  // rebuild without the root's upper-row slots
                 }
             }
