@@ -884,12 +884,16 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
                 }
                 // launch order of launch_group: the u8 staging (image read +
                 // staged columns written), generic K1, then K1P
-                if (g.nby > 0 && g.stage_img > 0)
+                // (u16 pair mode: the pass-0 output cell is 16 bits -- the
+                // minimum; the pair layout stores every row twice, which the
+                // ncu DRAM traffic shows as overhead)
+                const double e0 = g.pm_D ? 2.0 : ea;
+                if ((g.nby > 0 || g.pm_D) && g.stage_img > 0)
                     bytes.push_back(nimg * (static_cast<double>(plan->w) * plan->h + static_cast<double>(g.stage_img)));
-                if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : ea)));
-                if (g.nby > 0) bytes.push_back(slots * by_cols * H * (ein + ea));
+                if (g.nblocks > 0) bytes.push_back(slots * gen_cols * H * (ein + (g.sp.root_is_block ? eo : e0)));
+                if (g.nby > 0) bytes.push_back(slots * by_cols * H * (ein + e0));
                 for (size_t k = 0; k < g.sp.passes.size(); ++k)
-                    bytes.push_back(slots * g.sp.W * H * (ea + (k + 1 == g.sp.passes.size() ? eo : ea)));
+                    bytes.push_back(slots * g.sp.W * H * ((k == 0 ? e0 : ea) + (k + 1 == g.sp.passes.size() ? eo : ea)));
             }
         }
         for (int i = 0; i < n && i < max_launches && launch_bytes; ++i)

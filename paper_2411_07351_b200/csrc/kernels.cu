@@ -1466,6 +1466,37 @@ __device__ __forceinline__ void store_root_rows(Out* __restrict__ o, int W, int 
     }
 }
 
+// The same for tiles of at most 16 slopes: half-warps on two 4-row groups,
+// so every lane stores (a 16-slope tile otherwise idles half the warp).
+template <class Acc, class Out, int NWARPS>
+__device__ __forceinline__ void store_root_rows16(Out* __restrict__ o, int W, int t0, int nc, uint32_t sa, int r0,
+                                                  int rows, int warp, int lane) {
+    const int sub = lane >> 4, tl = lane & 15;
+    const size_t wstep = (size_t)W * (NWARPS * 8);
+    Out* __restrict__ prow = o + (size_t)(r0 + warp * 8 + sub * 4) * W + t0 + tl;
+    const uint32_t sl = sa + sub * 16u;
+    int i = warp * 8;
+    if (tl < nc) {
+        for (; i + 8 <= rows; i += NWARPS * 8, prow += wstep) {
+            const int4 v4 = lds4u(sl + i * 4u);
+            prow[0] = static_cast<Out>(from_bits<Acc>(v4.x));
+            prow[W] = static_cast<Out>(from_bits<Acc>(v4.y));
+            prow[2 * W] = static_cast<Out>(from_bits<Acc>(v4.z));
+            prow[3 * W] = static_cast<Out>(from_bits<Acc>(v4.w));
+        }
+        if (i < rows) {  // the last 1-7 rows
+            const int nr = rows - i - sub * 4;
+            if (nr > 0) {
+                const int4 v4 = lds4u(sl + i * 4u);
+                const int vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nr) prow[(size_t)k * W] = static_cast<Out>(from_bits<Acc>(vv[k]));
+            }
+        }
+    }
+}
+
 template <class Acc, class Out, int MODE>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
@@ -1583,8 +1614,14 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
                 for (int half = 0; half < (MODE == 6 ? 2 : 1); ++half) {
                     const int a0 = half ? x0r >> 16 : sl0, a1 = half ? x1r >> 16 : sl1;
                     const int r0 = half ? s0 + pmD : s0, nr = half ? rows_hi : rows;
-                    store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, smem_u32(sm + (size_t)a0 * L),
-                                                      smem_u32(sm + (size_t)a1 * L), r0, nr, warp, lane);
+                    if (nc <= 16) {  // lane l reads the slot of slope l & 15
+                        const int xs = __shfl_sync(0xffffffffu, half ? x0r >> 16 : sl0, lane & 15);
+                        store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, smem_u32(sm + (size_t)xs * L), r0, nr,
+                                                            warp, lane);
+                    } else {
+                        store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, smem_u32(sm + (size_t)a0 * L),
+                                                          smem_u32(sm + (size_t)a1 * L), r0, nr, warp, lane);
+                    }
                 }
             } else {
                 for (int i = warp; i < rows; i += kWarps) {
