@@ -386,6 +386,28 @@ __device__ __forceinline__ void rows_op_widen(uint32_t d, uint32_t dh, const uin
             }
     }
 }
+// rows_op_widen for exactly 256 words (a full pair-mode tile, the root has
+// no halo): 8 whole row groups with compile-time offsets, no predicates.
+template <int K, int SPLIT>
+__device__ __forceinline__ void rows_op_widen_256(uint32_t d, uint32_t dh, const uint32_t (&t)[4], int lane) {
+    const uint32_t lo = lane * 4u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        int v[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 256u * q + 128u * u);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            uint32_t x, y;
+            child_sums<K, SPLIT>(v[u], x, y);
+            sts1u(d + lo + 256u * q + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
+            sts1u(dh + lo + 256u * q + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
+        }
+    }
+}
+
 template <int NWARPS>
 __device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane) {
@@ -395,7 +417,8 @@ __device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __rest
         const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
                                base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
         const int n = h.y, nt = h.z & 7, split = q.w & 15;
-        if (nt == 4) rows_op_widen<4, 2>(d, dh, t, n, lane);
+        if (nt == 4 && n == 256) rows_op_widen_256<4, 2>(d, dh, t, lane);
+        else if (nt == 4) rows_op_widen<4, 2>(d, dh, t, n, lane);
         else if (nt == 2) rows_op_widen<2, 1>(d, dh, t, n, lane);
         else if (nt == 3 && split == 2) rows_op_widen<3, 2>(d, dh, t, n, lane);
         else if (nt == 3) rows_op_widen<3, 1>(d, dh, t, n, lane);

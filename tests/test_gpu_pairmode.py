@@ -91,3 +91,18 @@ def test_pair_mode_host_buffers():
         ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][i], ref[k])
+
+
+
+@pytest.mark.parametrize("bulk", [0, 1])
+def test_pair_mode_bulk_windows(monkeypatch, bulk):
+    """The pair-mode root band with its windows by cp.async or by TMA bulk copies."""
+    monkeypatch.setenv("FHT_K2_BULK", str(bulk))
+    rng = np.random.default_rng(10 + bulk)
+    imgs = rng.integers(0, 256, (5, 250, 333), dtype=np.uint8)
+    out, desc = _run(imgs, 1)
+    assert all(d > 0 for d in _pair_d(desc))
+    for i in (0, 2, 4):
+        ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"img{i} {k}")
