@@ -1398,6 +1398,16 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
             const Acc* col = in + (size_t)w.x * ld;
             const uint32_t d = stage + static_cast<uint32_t>(w.y) * L * 4u;
             const int start = wrap_any(s0 + w.z, H), n = S + w.w;
+            // common case: an aligned window that does not wrap -- whole
+            // 16-byte chunks, the last one rounded up (the <= 3 extra words
+            // land in the slot's slack; the read stays inside the column's ld)
+            const int n4 = (n + 3) & ~3;
+            if (!bar && (start & 3) == 0 && start + n <= H && start + n4 <= ld) {
+                const Acc* g = col + start + 4 * lane;
+                uint32_t sd = d + 16u * lane;
+                for (int k = lane; k < (n4 >> 2); k += 32, g += 128, sd += 512u) cp_async16(sd, g);
+                continue;
+            }
             // rows [start, H) then (past the wrap point) [0, n - (H - start)):
             // 16-byte copies while both sides are 16-byte aligned, 4-byte after
             const int na = min(n, H - start);

@@ -9,8 +9,9 @@ for a in sys.argv[3:]:
     name, rng = a.split(":")
     lo, hi = rng.split("-")
     regions.append((name, int(lo), int(hi)))
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "--kernel-name",
-                      f"regex:{kern}"], capture_output=True, text=True).stdout
+sel = ["--launch-skip", kern[5:], "--launch-count", "1"] if kern.startswith("skip:") else ["--kernel-name", f"regex:{kern}"]
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + sel,
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, data = None, []
 for r in rows:

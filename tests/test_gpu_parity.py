@@ -302,9 +302,11 @@ def test_profiled_launch_accounting(monkeypatch):
     # generic K1 (remainder block), K1P, root band
     assert kinds == [5, 1, 4, 3]
     slots, cells = 3 * 4, n * n
-    assert b[1] + b[2] == slots * cells * (1 + 4)  # pass 0 covers every column once: e_in + e_acc
-    assert b[2] == slots * (n // 32) * 32 * n * 5  # the 15 width-32 blocks
-    assert b[3] == slots * cells * 8
+    # the u16 pair mode is on for 509^2 u8: pass-0 cells are 16 bits
+    assert plan.describe()["groups"][0]["u16_pair_D"] == 256
+    assert b[1] + b[2] == slots * cells * (1 + 2)  # pass 0 covers every column once: e_in + e_pass0
+    assert b[2] == slots * (n // 32) * 32 * n * 3  # the 15 width-32 blocks
+    assert b[3] == slots * cells * (2 + 4)  # u16 cells in, int32 out
     pitch = plan.describe()["groups"][0]["stage_pitch"]
     assert pitch % 16 == 0 and pitch >= n + 31
     assert b[0] == 3 * (cells + 2 * n * pitch)  # image read + both staged column sets written
