@@ -1101,15 +1101,18 @@ __device__ __forceinline__ void by_level12_staged_pair(Acc* sm, int S, int tid, 
 }
 
 // Level 5 of the pair mode: words [0, D) stored from registers as in
-// by_level5_store, then words [D, H) formed with two shuffles per group.
-template <class Acc>
+// by_level5_store, then words [D, H) formed with one lane shuffle per group:
+// the source lane pre-selects the group the requesting lane needs (a lane
+// below e serves the next group's wrap-around).  DC: D known at compile time.
+template <class Acc, int DC = 0>
 __device__ __forceinline__ void by_level5_store_pair(Acc* sm, int warp, int lane, Acc* __restrict__ dcol0, int ld,
-                                                     int D, int H) {
+                                                     int D_, int H) {
     constexpr int w = 32, w0 = 16;
     constexpr int G = kBYMaxS / 32;  // D <= 256
+    const int D = DC ? DC : D_;
     const int e = 2 * D - H, nx = H - D;
     const int sl = (lane + e) & 31;
-    const bool same = lane + e < 32;
+    const bool wrap_src = lane < e;  // this lane's word is wanted by lane + 32 - e of the previous group
     const uint32_t base = smem_u32(sm) + lane * 4u;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
@@ -1135,8 +1138,8 @@ __device__ __forceinline__ void by_level5_store_pair(Acc* sm, int warp, int lane
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             if (32 * u >= nx) break;  // warp-uniform
-            const int s0v = __shfl_sync(0xffffffffu, v[u], sl), s1v = __shfl_sync(0xffffffffu, v[u + 1], sl);
-            if (32 * u + lane < nx) g[D + 32 * u] = from_bits<Acc>(pair_extra_word(v[u], same ? s0v : s1v));
+            const int hi = __shfl_sync(0xffffffffu, wrap_src ? v[u + 1] : v[u], sl);
+            if (32 * u + lane < nx) g[D + 32 * u] = from_bits<Acc>(pair_extra_word(v[u], hi));
         }
     }
 }
@@ -1182,7 +1185,9 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
                 by_level_s<Acc, 4>(sm, S, warp, lane);
             }
             __syncthreads();
-            by_level5_store_pair<Acc>(sm, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld, ld, pmD, H);
+            Acc* __restrict__ dcol0 = ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld;
+            if (pmD == kBYMaxS) by_level5_store_pair<Acc, kBYMaxS>(sm, warp, lane, dcol0, ld, pmD, H);
+            else by_level5_store_pair<Acc>(sm, warp, lane, dcol0, ld, pmD, H);
             return;
         }
         by_level12_staged<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
