@@ -1551,6 +1551,24 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     const int slot = blockIdx.z;
     const Acc* __restrict__ in = src + (size_t)slot * slot_elems;
 
+    // 1a. windows of the input columns, 4-byte types: cp.async, every window
+    // copy of the tile in flight at once, no register staging (16-byte copies
+    // before the wrap point, 4-byte after); issued first so that the op
+    // staging below overlaps their flight.  The bulk-copy mbarrier sits in
+    // the gap after the slots; one arrival per warp.
+    const uint32_t bar = (sizeof(Acc) == 4 && ps.bulk) ? smem_u32(sm + (size_t)ps.max_slots * L + 8) : 0u;
+    if constexpr (sizeof(Acc) == 4) {
+        if (bar) {
+            if (tid == 0) mbar_init(bar, kWarps);
+            __syncthreads();
+        }
+        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane, bar);
+        cp_async_commit();
+        if (bar) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar);
+        }
+    }
     // 0. stage the tile's merge ops in shared memory (after the slots)
     PassOpDev* sops = reinterpret_cast<PassOpDev*>(sm + (size_t)ps.max_slots * L + 16);
     int4* sbops = reinterpret_cast<int4*>(sops);
@@ -1565,22 +1583,8 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
         for (int k = tid; k < nops * 2; k += kThreads2)
             reinterpret_cast<int4*>(sops)[k] = reinterpret_cast<const int4*>(ps.ops + op0)[k];
     }
-    // 1. windows of the input columns
+    // 1b. the windows land (4-byte types) / are loaded through registers (8-byte)
     if constexpr (sizeof(Acc) == 4) {
-        // cp.async: every window copy of the tile in flight at once, no
-        // register staging (16-byte copies before the wrap point, 4-byte after)
-        // the mbarrier sits in the gap after the slots; one arrival per warp
-        const uint32_t bar = ps.bulk ? smem_u32(sm + (size_t)ps.max_slots * L + 8) : 0u;
-        if (bar) {
-            if (tid == 0) mbar_init(bar, kWarps);
-            __syncthreads();
-        }
-        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane, bar);
-        cp_async_commit();
-        if (bar) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar);
-        }
         cp_async_wait0();
         if (bar) mbar_wait(bar, 0);
     } else {
