@@ -265,7 +265,8 @@ void upload(Group& g) {
     }
     const size_t o_k1b = put(k1_bops.data(), k1_bops.size() * sizeof(int4));
     struct PassOff {
-        size_t tiles, loads, steps, ops, stores, bops;
+        size_t tiles, loads, steps, ops, stores, bops, bops1 = 0, stores1 = 0;
+        int pipe_delta = 0, pipe_loads = 0;
     };
     std::vector<PassOff> o_passes;
     for (const auto& ps : sp.passes) {
@@ -329,6 +330,50 @@ void upload(Group& g) {
                                          static_cast<int>(S + op.ext)));
             }
             o.bops = put(bops.data(), bops.size() * sizeof(int4));
+            // u16 pair mode root band: the second-buffer variant for the
+            // double-buffered kernel (load-space slots s < load_cnt -> s + delta)
+            const bool last = o_passes.size() + 1 == sp.passes.size();
+            if (g.pm_D && g.pairs && last && env_int("FHT_K2_PIPE", 1, 0, 1) == 1) {
+                const int delta = ps.pmax_slots;
+                int maxl = 0;
+                for (const auto& t : ps.ptiles) maxl = std::max(maxl, t.load_cnt);
+                std::vector<int4> b1 = bops;
+                std::vector<int2> st1 = stores;
+                auto mv = [&](int byteoff, int lc) {  // a baked byte offset slot*L*4 + off*4
+                    const int64_t sl = byteoff / (L * 4);
+                    return sl < lc ? static_cast<int>(byteoff + int64_t(delta) * L * 4) : byteoff;
+                };
+                for (const auto& t : ps.ptiles) {
+                    const int lc = t.load_cnt;
+                    const int ob = ps.pstep_offs[static_cast<size_t>(t.step_beg)];
+                    const int oe = ps.pstep_offs[static_cast<size_t>(t.step_beg + t.nsteps)];
+                    for (int oi = ob; oi < oe; ++oi) {
+                        const auto& op = ps.pops[static_cast<size_t>(oi)];
+                        int4& h = b1[2 * static_cast<size_t>(oi)];
+                        int4& q = b1[2 * static_cast<size_t>(oi) + 1];
+                        h.x = mv(h.x, lc);
+                        if (op.nterms > 0) h.w = mv(h.w, lc);
+                        if (op.nterms > 1) q.x = mv(q.x, lc);
+                        if (op.nterms > 2) q.y = mv(q.y, lc);
+                        if (op.nterms > 3) q.z = mv(q.z, lc);
+                        if (op.dst_hi >= 0) q.w = op.split | (mv(static_cast<int>(op.dst_hi * L * 4), lc) << 4);
+                    }
+                    for (int k = 0; k < t.store_cnt; ++k) {
+                        int2& r = st1[static_cast<size_t>(t.store_beg + k)];
+                        int lo = r.x & 0xffff, hi = r.x >> 16;
+                        if (lo < lc) lo += delta;
+                        if (hi < lc) hi += delta;
+                        if (lo >= (1 << 16) || hi >= (1 << 15)) throw FhtError(FHT_ERR_INTERNAL, "slot index overflow");
+                        r.x = lo | (hi << 16);
+                    }
+                }
+                const int64_t dh_max = int64_t(delta + maxl) * L * 4;
+                if (dh_max >= (int64_t(1) << 27)) throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
+                o.bops1 = put(b1.data(), b1.size() * sizeof(int4));
+                o.stores1 = put(st1.data(), st1.size() * sizeof(int2));
+                o.pipe_delta = delta;
+                o.pipe_loads = maxl;
+            }
         }
         o_passes.push_back(o);
     }
@@ -351,6 +396,12 @@ void upload(Group& g) {
         d.ops = reinterpret_cast<const fhtb::PassOpDev*>(base + o.ops);
         d.stores = reinterpret_cast<const int2*>(base + o.stores);
         d.bops = reinterpret_cast<const int4*>(base + o.bops);
+        d.bops1 = o.pipe_delta ? reinterpret_cast<const int4*>(base + o.bops1) : nullptr;
+        d.stores1 = o.pipe_delta ? reinterpret_cast<const int2*>(base + o.stores1) : nullptr;
+        d.pipe_delta = o.pipe_delta;
+        d.pipe_loads = o.pipe_loads;
+        d.tile_nc_max = 0;
+        for (const auto& t : program(sp.passes[i], g.pairs).tiles) d.tile_nc_max = std::max(d.tile_nc_max, t.store_cnt);
         d.S = g.pass_S[i];
         d.L = g.pass_L[i];
         const PassProgram pr = program(sp.passes[i], g.pairs);

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <set>
@@ -1706,6 +1707,78 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     }
 }
 
+// ------------------------------------------------------- K2, pair mode
+// The u16 pair mode root band with double-buffered windows: each CTA keeps
+// its tile and walks slots (grid.z strided).  While slot i computes, the
+// windows of slot i + 1 stream into the second buffer (load-space slots
+// moved by ps.pipe_delta; the op and store tables carry both variants), so
+// the copies' latency hides behind the merges.  Tiles of <= 16 slopes,
+// reference layout only (the launcher falls back to k2_pass MODE 6).
+template <class Out>
+__global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const int* __restrict__ src,
+                                                          long long slot_elems, int W, int H, int ld, OutDesc out,
+                                                          QuadSet qs, int img0, int pmD, int nslots) {
+    using Acc = int;
+    constexpr int kWarps = kThreads2 / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Acc* sm = reinterpret_cast<Acc*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const PassTileDev tile = ps.tiles[blockIdx.y];
+    const int S = ps.S, L = ps.L;
+    const int s0 = blockIdx.x * S;
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t alt = static_cast<uint32_t>(ps.pipe_delta) * static_cast<uint32_t>(L) * 4u;
+    int slot = blockIdx.z;
+    // the tile's op tables (both buffers) and step offsets, then the first
+    // slot's windows (those wait for the previous kernel)
+    int4* sbops = reinterpret_cast<int4*>(sm + (size_t)(ps.pipe_delta + ps.pipe_loads) * L + 16);
+    const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
+    int* ssteps = reinterpret_cast<int*>(sbops + 4 * ps.max_tile_ops);
+    if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid] - op0;
+    for (int k = tid; k < 2 * nops; k += kThreads2) {
+        sbops[k] = ps.bops[2 * op0 + k];
+        sbops[2 * nops + k] = ps.bops1[2 * op0 + k];
+    }
+    const int nc = tile.store_cnt;
+    const int t0 = ps.stores[tile.store_beg].y;
+    const int xs0 = (lane & 15) < nc ? ps.stores[tile.store_beg + (lane & 15)].x : 0;
+    const int xs1 = (lane & 15) < nc ? ps.stores1[tile.store_beg + (lane & 15)].x : 0;
+    const int rows = min(S, pmD - s0), rows_hi = max(0, min(rows, H - pmD - s0));
+    grid_dep_wait();
+    issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u);
+    cp_async_commit();
+    for (int it = 0;; ++it) {
+        const int p = it & 1;
+        cp_async_wait0();  // this slot's windows
+        __syncthreads();   // ... visible to all; the last slot's store is done with the other buffer
+        const int next = slot + static_cast<int>(gridDim.z);
+        if (next < nslots) {
+            issue_windows<Acc>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H, ld,
+                               warp, lane, 0u);
+            cp_async_commit();
+        }
+        const int4* ops = sbops + (p ? 2 * nops : 0);
+        for (int k = 0; k < tile.nsteps; ++k) {
+            if (k) __syncthreads();
+            if (k + 1 < tile.nsteps) run_step_terms<Acc, kWarps, false>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+            else run_step_widen<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+        }
+        __syncthreads();
+        int img_l, qi;
+        split_slot(slot, qs.n, img_l, qi);
+        Out* __restrict__ o =
+            reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
+        const int xs = p ? xs1 : xs0;
+        store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs & 0xffff) * L * 4u, s0,
+                                            rows, warp, lane);
+        if (rows_hi > 0)
+            store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs >> 16) * L * 4u,
+                                                s0 + pmD, rows_hi, warp, lane);
+        slot = next;
+        if (slot >= nslots) break;
+    }
+}
+
 // ------------------------------------------------------------ root merge
 // The root level from its two children held as separate slope-major column
 // ranges (the multi-GPU root split): output slopes [t_beg,
@@ -1773,6 +1846,11 @@ void allow_smem(const void* fn) {
     std::lock_guard<std::mutex> lk(mu);
     if (done.insert({dev, fn}).second)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+int env_slots_per_cta() {
+    const char* e = std::getenv("FHT_K2_SLOTS_PER_CTA");
+    return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
 }
 
 template <class In, class Acc, class Out>
@@ -1857,6 +1935,24 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         }
         PassDev pd = ps;
         pd.bulk = g.k2_bulk;
+        if constexpr (std::is_same<Acc, int32_t>::value) {
+            // pair-mode root band with double-buffered windows
+            int max_nc = 0;
+            (void)max_nc;
+            if (g.pm_D && final_pass && ps.pairs && ps.pipe_delta > 0 && !g.k2_bulk && g.out.layout == 0 &&
+                ps.tile_nc_max <= 16) {
+                const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops);
+                auto kp = k2_pair_pipe<Out>;
+                allow_smem(reinterpret_cast<const void*>(kp));
+                const int spc = env_slots_per_cta();
+                dim3 gp(((g.pm_D) + ps.S - 1) / ps.S, ps.ntiles, (nslots + spc - 1) / spc);
+                launch_k(g.pdl, kp, gp, dim3(kThreads2), smp, st, pd, SRC, slot_elems, g.W, g.H, g.ld, g.out, g.qs,
+                         g.img0, g.pm_D, nslots);
+                ++launches;
+                if (hook) hook(ctx, 3);
+                continue;
+            }
+        }
         allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2(((g.pm_D ? g.pm_D : g.H) + ps.S - 1) / ps.S, ps.ntiles, nslots);
         launch_k(g.pdl, k2, g2, dim3(kThreads2), smem2, st, pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out,

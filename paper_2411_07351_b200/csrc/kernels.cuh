@@ -61,6 +61,13 @@ struct PassDev {
     int max_tile_ops;  // most merge ops in one tile (staged in shared memory)
     int bulk;          // window runs by TMA bulk copies (set per launch)
     int pairs;         // the tables are level-pair programs (bops: 2 records per op)
+    // u16 pair mode root band, double-buffered windows (k2_pair_pipe): the same
+    // ops / stores with every load-space slot s < tile.load_cnt moved to
+    // s + pipe_delta (the second window buffer); pipe_delta = 0: no such tables
+    const int4* bops1;
+    const int2* stores1;
+    int pipe_delta, pipe_loads;  // slot offset of the second buffer, its size (max load_cnt)
+    int tile_nc_max;             // most stored slopes of one tile
 };
 
 struct GroupLaunch {

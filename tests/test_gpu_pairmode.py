@@ -106,3 +106,20 @@ def test_pair_mode_bulk_windows(monkeypatch, bulk):
         ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"img{i} {k}")
+
+
+@pytest.mark.parametrize("pipe,spc", [(1, 1), (1, 3), (1, 64), (0, 4)])
+def test_pair_mode_double_buffered_root_band(monkeypatch, pipe, spc):
+    """k2_pair_pipe: each CTA walks `spc` slots with the next slot's windows
+    streaming into the second buffer (FHT_K2_PIPE=0: one slot per CTA)."""
+    monkeypatch.setenv("FHT_K2_PIPE", str(pipe))
+    monkeypatch.setenv("FHT_K2_SLOTS_PER_CTA", str(spc))
+    rng = np.random.default_rng(100 + spc)
+    imgs = rng.integers(0, 256, (7, 509, 509), dtype=np.uint8)
+    imgs[3] = 255
+    out, desc = _run(imgs, 1)
+    assert _pair_d(desc) == [256]
+    for i in (0, 3, 5, 6):
+        ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"img{i} {k}")
