@@ -1848,9 +1848,14 @@ void allow_smem(const void* fn) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-int env_slots_per_cta() {
-    const char* e = std::getenv("FHT_K2_SLOTS_PER_CTA");
-    return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
+// Slots one k2_pair_pipe CTA walks: FHT_K2_SLOTS_PER_CTA, else as many as
+// keep >= 4 waves of 2 CTAs per SM, at most 8 (measured best for c4).
+int slots_per_cta(int ctas_at_one, int nslots) {
+    if (const char* e = std::getenv("FHT_K2_SLOTS_PER_CTA")) return std::max(1, std::min(64, std::atoi(e)));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 4)}));
 }
 
 template <class In, class Acc, class Out>
@@ -1944,8 +1949,9 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                 const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops);
                 auto kp = k2_pair_pipe<Out>;
                 allow_smem(reinterpret_cast<const void*>(kp));
-                const int spc = env_slots_per_cta();
-                dim3 gp(((g.pm_D) + ps.S - 1) / ps.S, ps.ntiles, (nslots + spc - 1) / spc);
+                const int rt = (g.pm_D + ps.S - 1) / ps.S;
+                const int spc = slots_per_cta(rt * ps.ntiles * nslots, nslots);
+                dim3 gp(rt, ps.ntiles, (nslots + spc - 1) / spc);
                 launch_k(g.pdl, kp, gp, dim3(kThreads2), smp, st, pd, SRC, slot_elems, g.W, g.H, g.ld, g.out, g.qs,
                          g.img0, g.pm_D, nslots);
                 ++launches;
