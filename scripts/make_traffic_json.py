@@ -21,6 +21,8 @@ def parse(path: pathlib.Path):
             cur = m.group(1)
             if cur == "k1_by32":
                 cur = "k1p_by32"
+            if cur == "k2_pair_pipe":  # the pair-mode root band (double-buffered windows)
+                cur = "k2_pass_root"
             if cur == "k2_pass":
                 k2 += 1
                 cur = "k2_pass" if k2 == 1 else "k2_pass_root"
