@@ -356,20 +356,28 @@ void build_tile(const std::vector<Node>& nodes, const std::vector<char>& front, 
                         self(self, md.child[1], t1, shift + r, step_of(md.child[1]) >= gs && m == n);
                     };
                     add_terms(add_terms, n, t, 0, true);
-                    if (pfree.empty()) {
-                        op.dst = pnext++;
-                    } else {
-                        op.dst = pfree.back();
-                        pfree.pop_back();
-                    }
+                    // A stored column prefers a freed slot of index == its slope mod 8:
+                    // the root store reads 16-32 of them at one row offset, and with
+                    // every residue equally often (slot stride L, L/4 odd) the reads
+                    // spread evenly over the shared-memory banks.
+                    auto take = [&](int want) {
+                        if (pfree.empty()) return pnext++;
+                        size_t pick = pfree.size() - 1;
+                        if (want >= 0)
+                            for (size_t k = pfree.size(); k-- > 0;)
+                                if ((pfree[k] & 7) == want) {
+                                    pick = k;
+                                    break;
+                                }
+                        const int sl = pfree[pick];
+                        pfree.erase(pfree.begin() + static_cast<std::ptrdiff_t>(pick));
+                        return sl;
+                    };
+                    const int want = n == X ? (t - ta) & 7 : -1;
+                    op.dst = take(want);
                     pslot[static_cast<size_t>(n)][static_cast<size_t>(t)] = op.dst;
                     if (ps.root_hi && X == 0 && n == X) {  // the widened root's upper rows
-                        if (pfree.empty()) {
-                            op.dst_hi = pnext++;
-                        } else {
-                            op.dst_hi = pfree.back();
-                            pfree.pop_back();
-                        }
+                        op.dst_hi = take(want);
                         phi[static_cast<size_t>(t)] = op.dst_hi;
                     }
                     ps.pops.push_back(op);
