@@ -1066,15 +1066,15 @@ __device__ __forceinline__ void by_level12_staged(Acc* sm, int S, int tid, const
 
 // by_level12_staged in the u16 pair mode: the leaf words pack rows 4j.. of
 // the low half with rows 4j + D.. of the high half (both aligned: D % 4 == 0).
-template <class Acc>
+template <class Acc, int GT = 64>
 __device__ __forceinline__ void by_level12_staged_pair(Acc* sm, int S, int tid, const unsigned char* __restrict__ sb,
                                                        long long spitch, int W, int x0, bool rev, int D) {
     const int nchunk = (S + kBYW - 4 + 3) >> 2;
     int4* O = reinterpret_cast<int4*>(sm);
     constexpr int s4 = kBYSR / 4;
-    const int g = tid >> 6;
+    const int g = tid / GT;  // GT threads per 4-column group
     const int dw = D >> 2;  // the high half, in 4-byte words
-    for (int j = tid & 63; j < nchunk; j += 64) {
+    for (int j = tid - g * GT; j < nchunk; j += GT) {
         const int c = x0 + 4 * g;
         const long long cs = rev ? -spitch : spitch;
         const unsigned char* pa = sb + (long long)(rev ? W - 1 - c : c) * spitch + 4 * j;
@@ -1330,6 +1330,47 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     for (int h = 0; h < 2; ++h) {
         const int c = warp + h * kWarpsBY;
         warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, root + c * kBYSR, rows_out, al, lane);
+    }
+}
+
+// K1P of the u16 pair mode on 576 threads: 8 column groups x 72 threads
+// take the 71 level-2 row chunks of a 256-word tile in one round (with 512
+// threads, 7 of each group's 64 threads ran a second item that the whole
+// CTA then waited for); levels 3-5 run on warps 0-15 as in k1_by32.
+// 56 registers keep two CTAs per SM.
+constexpr int kThreadsBYP = 576;
+template <class Acc>
+__global__ void __launch_bounds__(kThreadsBYP, 2) k1_by32_pair(QuadSet qs, int W, int H, int ld, int S,
+                                                                const int* __restrict__ bx0, Acc* __restrict__ ws,
+                                                                int nbuf, const unsigned char* __restrict__ stage,
+                                                                long long spitch, long long simg, long long st_t,
+                                                                long long st_p, int pmD) {
+    grid_dep_wait();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Acc* sm = reinterpret_cast<Acc*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int x0 = bx0[blockIdx.y];
+    const int slot = blockIdx.z;
+    int img_l, qi;
+    split_slot(slot, qs.n, img_l, qi);
+    const int q = quad_code(qs, qi);
+    const unsigned char* __restrict__ sb = stage + (size_t)img_l * simg + (q < 2 ? st_t : st_p);
+    by_level12_staged_pair<Acc, kThreadsBYP / 8>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0, pmD);
+    __syncthreads();
+    if (warp < kWarpsBY) {
+        if (S == kBYMaxS) by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
+        else by_level_s<Acc, 3>(sm, S, warp, lane);
+    }
+    __syncthreads();
+    if (warp < kWarpsBY) {
+        if (S == kBYMaxS) by_level_s<Acc, 4, 0, kBYMaxS>(sm, S, warp, lane);
+        else by_level_s<Acc, 4>(sm, S, warp, lane);
+    }
+    __syncthreads();
+    if (warp < kWarpsBY) {
+        Acc* __restrict__ dcol0 = ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld;
+        if (pmD == kBYMaxS) by_level5_store_pair<Acc, kBYMaxS>(sm, warp, lane, dcol0, ld, pmD, H);
+        else by_level5_store_pair<Acc>(sm, warp, lane, dcol0, ld, pmD, H);
     }
 }
 
@@ -1908,11 +1949,24 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                       : g.k1p_variant == 4 ? k1_by32<In, Acc, 4>
                                            : k1_by32<In, Acc, 5>;
             const int sm_by = static_cast<int>(k1_by32_smem_bytes());
-            allow_smem(reinterpret_cast<const void*>(kb));
-            dim3 gb(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nby, nslots);
-            launch_k(g.pdl, kb, gb, dim3(kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w, g.img_h,
-                     g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf, stage,
-                     g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, stage ? g.pm_D : 0);
+            bool launched = false;
+            if constexpr (std::is_same<In, unsigned char>::value && std::is_same<Acc, int32_t>::value) {
+                // the pair mode's K1P: 576 threads (FHT_K1P_PAIR576=0: the 512-thread kernel)
+                if (g.pm_D && stage && g.k1p_pair576) {
+                    auto kq = k1_by32_pair<Acc>;
+                    allow_smem(reinterpret_cast<const void*>(kq));
+                    launch_k(g.pdl, kq, dim3(1, g.nby, nslots), dim3(kThreadsBYP), sm_by, st, g.qs, g.W, g.H, g.ld, g.S,
+                             g.by_x0, ws, g.nbuf, stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D);
+                    launched = true;
+                }
+            }
+            if (!launched) {
+                allow_smem(reinterpret_cast<const void*>(kb));
+                dim3 gb(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nby, nslots);
+                launch_k(g.pdl, kb, gb, dim3(kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w,
+                         g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf,
+                         stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, stage ? g.pm_D : 0);
+            }
             ++launches;
             if (hook) hook(ctx, 4);
         }

@@ -119,6 +119,7 @@ struct GroupLaunch {
     // u16 pair mode (0: off): workspace words hold rows (j, j + pm_D);
     // K1/K1P/K2 run one row tile of pm_D words, K2's root step widens to 32 bits
     int pm_D;
+    int k1p_pair576;  // pair mode: K1P on 576 threads (one round of level-1/2 items)
     unsigned char* stage;
     long long stage_pitch, stage_img;
     long long stage_t, stage_p;  // byte offsets inside an image's stage (-1: not staged)

@@ -123,3 +123,19 @@ def test_pair_mode_double_buffered_root_band(monkeypatch, pipe, spc):
         ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"img{i} {k}")
+
+
+@pytest.mark.parametrize("k576", [0, 1])
+def test_pair_mode_k1p_thread_counts(monkeypatch, k576):
+    """The pair mode's K1P on 576 threads (one round of level-1/2 items) and on
+    the 512-thread kernel, for odd and even heights."""
+    monkeypatch.setenv("FHT_K1P_PAIR576", str(k576))
+    rng = np.random.default_rng(5 + k576)
+    for h, w in [(509, 509), (400, 256), (129, 300)]:
+        imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)
+        out, desc = _run(imgs, 1)
+        assert all(d > 0 for d in _pair_d(desc))
+        for i in range(2):
+            ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
+            for k in Q:
+                np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"{h}x{w} img{i} {k}")
