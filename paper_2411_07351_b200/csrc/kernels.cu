@@ -753,14 +753,17 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
     const bool want_p = off_p >= 0 && r0 < h && c0 < pitch_p;
     if (!want_t && !want_p) return;
     const unsigned char* __restrict__ base = img + (size_t)(img0 + im) * img_stride;
-    if (c0 + 64 <= w && r0 + 64 <= h) {
-        // interior tile: each row segment read as aligned 4-byte words (two
-        // per 4 pixels, funnel-shifted into place), 4 words per thread
+    if (c0 + 64 <= w) {
+        // columns in range (rows may wrap: the staged columns run past h):
+        // each row segment read as aligned 4-byte words (two per 4 pixels,
+        // funnel-shifted into place), 4 words per thread
         const int j = threadIdx.x & 15, rr0 = threadIdx.x >> 4;  // word j of rows rr0, rr0 + 16, ...
         uint32_t v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const unsigned char* p = base + (size_t)(r0 + rr0 + 16 * k) * pitch + c0 + 4 * j;
+            int r = r0 + rr0 + 16 * k;
+            if (r >= h) r = r - h < h ? r - h : r % h;  // the wrapped head rows
+            const unsigned char* p = base + (size_t)r * pitch + c0 + 4 * j;
             const uint32_t* a = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
             const uint32_t sh = 8u * static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) & 3);
             v[k] = __funnelshift_r(__ldg(a), sh ? __ldg(a + 1) : 0u, sh);

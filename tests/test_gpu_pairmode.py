@@ -139,3 +139,32 @@ def test_pair_mode_k1p_thread_counts(monkeypatch, k576):
             ref, _ = oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)
             for k in Q:
                 np.testing.assert_array_equal(out[k][i], ref[k], err_msg=f"{h}x{w} img{i} {k}")
+
+
+def test_pair_mode_chunks_and_graph_replay(monkeypatch):
+    """Pair mode over image chunks (FHT_CHUNK_IMAGES: per-chunk staging and
+    slot offsets) and replayed from a captured CUDA graph."""
+    monkeypatch.setenv("FHT_CHUNK_IMAGES", "3")
+    rng = np.random.default_rng(21)
+    imgs = rng.integers(0, 256, (7, 509, 509), dtype=np.uint8)
+    plan = fht.Plan(509, 509, 1, in_dtype="u8", acc_dtype="i32", quadrants="all", batch=7)
+    assert plan.describe()["chunk"] == 3
+    x = torch.from_numpy(imgs).cuda()
+    out = plan.alloc_outputs()
+    plan(x, out)
+    torch.cuda.synchronize()
+    refs = {i: oracle.fht2d_quadrants(imgs[i], 1, dtype=np.int32)[0] for i in (0, 3, 6)}
+    for i, ref in refs.items():
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i].cpu().numpy(), ref[k], err_msg=f"chunked img{i} {k}")
+    for v in out.values():
+        v.zero_()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan(x, out, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    for i, ref in refs.items():
+        for k in Q:
+            np.testing.assert_array_equal(out[k][i].cpu().numpy(), ref[k], err_msg=f"graph img{i} {k}")
