@@ -753,7 +753,9 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
     const bool want_p = off_p >= 0 && r0 < h && c0 < pitch_p;
     if (!want_t && !want_p) return;
     const unsigned char* __restrict__ base = img + (size_t)(img0 + im) * img_stride;
-    if (c0 + 64 <= w) {
+    // a tile wholly past column w holds wrapped columns c0 - w.. (the P set)
+    const int cs0 = c0 < w ? c0 : c0 - w;
+    if (cs0 + 64 <= w && (c0 < w || c0 - w < w)) {
         // columns in range (rows may wrap: the staged columns run past h):
         // each row segment read as aligned 4-byte words (two per 4 pixels,
         // funnel-shifted into place), 4 words per thread
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
         for (int k = 0; k < 4; ++k) {
             int r = r0 + rr0 + 16 * k;
             if (r >= h) r = r - h < h ? r - h : r % h;  // the wrapped head rows
-            const unsigned char* p = base + (size_t)r * pitch + c0 + 4 * j;
+            const unsigned char* p = base + (size_t)r * pitch + cs0 + 4 * j;
             const uint32_t* a = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
             const uint32_t sh = 8u * static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) & 3);
             v[k] = __funnelshift_r(__ldg(a), sh ? __ldg(a + 1) : 0u, sh);
