@@ -199,6 +199,14 @@ __device__ __forceinline__ int lds1u(uint32_t a) {
 __device__ __forceinline__ void sts1u(uint32_t a, int v) {
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// An address the compiler must treat as opaque: the inner loops add only
+// compile-time offsets to it, which ptxas folds into the LDS/STS immediate.
+// (Otherwise NVVM rewrites t[k] + lane*4 + c as t[k] + (lane*4 | c) to share
+// the OR across terms -- one extra IADD per shared load.)
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm("" : "+r"(x));
+    return x;
+}
 template <class Acc>
 __device__ __forceinline__ int add_bits(int x, int y) {
     return to_bits<Acc>(from_bits<Acc>(x) + from_bits<Acc>(y));
@@ -262,24 +270,28 @@ template <class Acc, int K, int SPLIT>
 __device__ __forceinline__ void rows_op_terms(uint32_t d, const uint32_t (&t)[4], int n, int lane) {
     constexpr int U = 4;
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
+    const uint32_t dd = opaque(d + lo);
     int i0 = 0;
     for (; i0 + 32 * U <= n; i0 += 32 * U) {
         int v[U][4];
-        const uint32_t o = lo + i0 * 4u;
+        const uint32_t o = i0 * 4u;
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + o + 128u * u);
 #pragma unroll
-        for (int u = 0; u < U; ++u) sts1u(d + o + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
+        for (int u = 0; u < U; ++u) sts1u(dd + o + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
     }
     for (; i0 < n; i0 += 32)
         if (i0 + lane < n) {
-            const uint32_t o = lo + i0 * 4u;
+            const uint32_t o = i0 * 4u;
             int v[4];
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + o);
-            sts1u(d + o, sum_terms<Acc, K, SPLIT>(v));
+            for (int k = 0; k < K; ++k) v[k] = lds1u(p[k] + o);
+            sts1u(dd + o, sum_terms<Acc, K, SPLIT>(v));
         }
 }
 
@@ -289,23 +301,26 @@ template <class Acc, int K, int SPLIT>
 __device__ __forceinline__ void rows_op_terms_global(Acc* __restrict__ g, const uint32_t (&t)[4], int n, int lane) {
     constexpr int U = 4;
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
     int i0 = 0;
     for (; i0 + 32 * U <= n; i0 += 32 * U) {
         int v[U][4];
-        const uint32_t o = lo + i0 * 4u;
+        const uint32_t o = i0 * 4u;
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + o + 128u * u);
 #pragma unroll
         for (int u = 0; u < U; ++u) g[i0 + 32 * u + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v[u]));
     }
     for (; i0 < n; i0 += 32)
         if (i0 + lane < n) {
-            const uint32_t o = lo + i0 * 4u;
+            const uint32_t o = i0 * 4u;
             int v[4];
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + o);
+            for (int k = 0; k < K; ++k) v[k] = lds1u(p[k] + o);
             g[i0 + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v));
         }
 }
@@ -316,21 +331,25 @@ __device__ __forceinline__ void rows_op_terms_global(Acc* __restrict__ g, const 
 template <class Acc, int K, int SPLIT>
 __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t)[4], int n, int lane) {
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
+    const uint32_t dd = opaque(d + lo);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         int v[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 512u * half + 128u * u);
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + 512u * half + 128u * u);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) sts1u(d + lo + 512u * half + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
+        for (int u = 0; u < 4; ++u) sts1u(dd + 512u * half + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
     }
     if (256 + lane < n) {
         int v[4];
 #pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = lds1u(t[k] + lo + 1024u);
-        sts1u(d + lo + 1024u, sum_terms<Acc, K, SPLIT>(v));
+        for (int k = 0; k < K; ++k) v[k] = lds1u(p[k] + 1024u);
+        sts1u(dd + 1024u, sum_terms<Acc, K, SPLIT>(v));
     }
 }
 
@@ -338,13 +357,16 @@ __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t
 template <class Acc, int K, int SPLIT>
 __device__ __forceinline__ void rows_op_terms_global_256(Acc* __restrict__ g, const uint32_t (&t)[4], int lane) {
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         int v[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 512u * half + 128u * u);
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + 512u * half + 128u * u);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             g[128 * half + 32 * u + lane] = from_bits<Acc>(sum_terms<Acc, K, SPLIT>(v[u]));
@@ -369,21 +391,25 @@ template <int K, int SPLIT>
 __device__ __forceinline__ void rows_op_widen(uint32_t d, uint32_t dh, const uint32_t (&t)[4], int n, int lane) {
     constexpr int U = 2;
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
+    const uint32_t dd = opaque(d + lo), ddh = opaque(dh + lo);
     for (int i0 = 0; i0 < n; i0 += 32 * U) {
         int v[U][4];
-        const uint32_t o = lo + i0 * 4u;
+        const uint32_t o = i0 * 4u;
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (i0 + 32 * u + lane < n)
 #pragma unroll
-                for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + o + 128u * u);
+                for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + o + 128u * u);
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (i0 + 32 * u + lane < n) {
                 uint32_t x, y;
                 child_sums<K, SPLIT>(v[u], x, y);
-                sts1u(d + o + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
-                sts1u(dh + o + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
+                sts1u(dd + o + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
+                sts1u(ddh + o + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
             }
     }
 }
@@ -392,19 +418,23 @@ __device__ __forceinline__ void rows_op_widen(uint32_t d, uint32_t dh, const uin
 template <int K, int SPLIT>
 __device__ __forceinline__ void rows_op_widen_256(uint32_t d, uint32_t dh, const uint32_t (&t)[4], int lane) {
     const uint32_t lo = lane * 4u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
+    const uint32_t dd = opaque(d + lo), ddh = opaque(dh + lo);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         int v[2][4];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int k = 0; k < K; ++k) v[u][k] = lds1u(t[k] + lo + 256u * q + 128u * u);
+            for (int k = 0; k < K; ++k) v[u][k] = lds1u(p[k] + 256u * q + 128u * u);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             uint32_t x, y;
             child_sums<K, SPLIT>(v[u], x, y);
-            sts1u(d + lo + 256u * q + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
-            sts1u(dh + lo + 256u * q + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
+            sts1u(dd + 256u * q + 128u * u, static_cast<int>((x & 0xffffu) + (y & 0xffffu)));
+            sts1u(ddh + 256u * q + 128u * u, static_cast<int>((x >> 16) + (y >> 16)));
         }
     }
 }
