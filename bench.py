@@ -192,12 +192,14 @@ def run_reference(args):
     c = workloads.CONFIGS[args.config]
     strategy = 0 if args.strategy == "simple" else 1
     threads = oracle.host_threads()
+    # each step: whole rounds of one image per host thread for at least
+    # 0.5 s (a 0.04 s step was too short for a stable median)
     for _ in range(args.warmup):
         cpu_baseline(args.config, strategy, 0.0, threads)
     per_step = []
     vals = []
     for _ in range(args.steps):
-        r = cpu_baseline(args.config, strategy, 0.0, threads)
+        r = cpu_baseline(args.config, strategy, 0.5, threads)
         vals.append(r["value"])
         per_step.append(r)
     value = statistics.median(vals)

@@ -19,7 +19,7 @@ def parse(path: pathlib.Path):
         m = re.match(r"raw \[.*::(k\w+)", line)
         if m:
             cur = m.group(1)
-            if cur == "k1_by32":
+            if cur in ("k1_by32", "k1_by32_pair"):  # k1_by32_pair: the u16 pair-mode K1P
                 cur = "k1p_by32"
             if cur == "k2_pair_pipe":  # the pair-mode root band (double-buffered windows)
                 cur = "k2_pass_root"
