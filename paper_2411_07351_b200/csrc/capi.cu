@@ -658,6 +658,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.k1p_variant = g.pm_D ? 5 : env_int("FHT_K1P_VARIANT", 5, 0, 5);  // see GroupLaunch
             L.pm_D = g.pm_D;
             L.k1p_pair576 = env_int("FHT_K1P_PAIR576", 1, 0, 1);
+            L.k1p_576 = env_int("FHT_K1P_576", 1, 0, 1);
             L.k2_scalar = env_int("FHT_K2_SCALAR", 1, 0, 1);
             L.k2_bulk = env_int("FHT_K2_BULK", 0, 0, 1);
             L.pdl = env_int("FHT_PDL", 1, 0, 1);

@@ -869,6 +869,11 @@ constexpr int kBYSR = 300;      // slot stride: >= 256 + 31 + 12, multiple of 4,
 constexpr int kThreadsBY = 512;
 static_assert(kThreadsBY == 8 * 64, "levels 1-2 map 8 column groups x 64 threads");
 constexpr int kWarpsBY = kThreadsBY / 32;
+// K1P on 576 threads: 8 column groups x 72 threads take the 71 level-2 row
+// chunks of a 256-row tile in one round (with 512 threads, 7 of each group's
+// 64 threads ran a second item that the whole CTA then waited for); the
+// leaves and levels 3-5 stay on warps 0-15.  56 registers keep two CTAs/SM.
+constexpr int kThreadsBYP = 576;
 
 // Level L (1..5) merges widths 2^(L-1) -> 2^L.  For block-local column T
 // the children's slope t0 = t1 = rhu(tl (w0-1), w-1) (split.hpp:53-57) is
@@ -930,7 +935,7 @@ __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
 // from registers); full 256-row tiles take the compile-time row count.
 template <class Acc>
 __device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
-                                              int rows_out);
+                                              int rows_out, bool act = true);
 
 // Level 5 (the block root) written straight to the pass-0 buffer from
 // registers: lane = row, so each warp store is 32 consecutive rows of one
@@ -966,17 +971,18 @@ __device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int la
 
 template <class Acc>
 __device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
-                                              int rows_out) {
+                                              int rows_out, bool act) {
     if (S == kBYMaxS) {
-        by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
+        if (act) by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
         __syncthreads();
-        by_level_s<Acc, 4, 0, kBYMaxS>(sm, S, warp, lane);  // -> slots [0, 32)
+        if (act) by_level_s<Acc, 4, 0, kBYMaxS>(sm, S, warp, lane);  // -> slots [0, 32)
     } else {
-        by_level_s<Acc, 3>(sm, S, warp, lane);
+        if (act) by_level_s<Acc, 3>(sm, S, warp, lane);
         __syncthreads();
-        by_level_s<Acc, 4>(sm, S, warp, lane);
+        if (act) by_level_s<Acc, 4>(sm, S, warp, lane);
     }
     __syncthreads();
+    if (!act) return;
     if (rows_out == kBYMaxS)  // a full tile (the last row tile may be shorter)
         by_level5_store<Acc, kBYMaxS>(sm, S, warp, lane, dcol0, ld, rows_out);
     else
@@ -1026,16 +1032,14 @@ __device__ __forceinline__ int4 shifted(int4 lo, int4 hi) {
     return make_int4(v[K], v[K + 1], v[K + 2], v[K + 3]);
 }
 
-template <class Acc>
+template <class Acc, int GT = 64>
 __device__ __forceinline__ void by_level12(Acc* sm, int S, int tid) {
     const int nchunk = (S + kBYW - 4 + 3) >> 2;  // row chunks of 4 the level-2 output needs
-    const int items = 8 * nchunk;
     const int4* V = reinterpret_cast<const int4*>(sm);
     int4* O = reinterpret_cast<int4*>(sm);
     constexpr int s4 = kBYSR / 4;
-    (void)items;
-    const int g = tid >> 6;  // 8 column groups x 64 threads; lanes over row chunks: conflict-free
-    for (int j = tid & 63; j < nchunk; j += 64) {
+    const int g = tid / GT;  // 8 column groups x GT threads; lanes over row chunks: conflict-free
+    for (int j = tid - g * GT; j < nchunk; j += GT) {
         const int c0 = (kBYW + 4 * g) * s4 + j;  // leaves of column 4g, chunk j
         // pair (4g, 4g+1) -> level-1 columns p0 (shift 0), p1 (shift 1), rows j*4 .. j*4+6
         const int4 a0 = V[c0], a1 = V[c0 + 1], b0 = V[c0 + s4], b1 = V[c0 + s4 + 1];
@@ -1065,16 +1069,14 @@ __device__ __forceinline__ int4 unpack_u8x4(uint32_t x) {
     return make_int4(to_bits<Acc>(static_cast<Acc>(x & 0xff)), to_bits<Acc>(static_cast<Acc>((x >> 8) & 0xff)),
                      to_bits<Acc>(static_cast<Acc>((x >> 16) & 0xff)), to_bits<Acc>(static_cast<Acc>(x >> 24)));
 }
-template <class Acc>
+template <class Acc, int GT = 64>
 __device__ __forceinline__ void by_level12_staged(Acc* sm, int S, int tid, const unsigned char* __restrict__ sb,
                                                   long long spitch, int W, int x0, bool rev) {
     const int nchunk = (S + kBYW - 4 + 3) >> 2;
-    const int items = 8 * nchunk;
     int4* O = reinterpret_cast<int4*>(sm);
     constexpr int s4 = kBYSR / 4;
-    (void)items;
-    const int g = tid >> 6;  // 8 column groups x 64 threads, lanes over consecutive row chunks
-    for (int j = tid & 63; j < nchunk; j += 64) {
+    const int g = tid / GT;  // 8 column groups x GT threads, lanes over consecutive row chunks
+    for (int j = tid - g * GT; j < nchunk; j += GT) {
         const int c = x0 + 4 * g;
         const long long cs = rev ? -spitch : spitch;  // reversed column order for horiz_neg / vert_neg
         const unsigned char* pa = sb + (long long)(rev ? W - 1 - c : c) * spitch + 4 * j;
@@ -1181,8 +1183,8 @@ __device__ __forceinline__ void by_level5_store_pair(Acc* sm, int warp, int lane
 }
 
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
-template <class In, class Acc, int V>
-__global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
+template <class In, class Acc, int V, int NT = kThreadsBY>
+__global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
                                                           long long img_pitch, long long img_stride, int img0, QuadSet qs, int W, int H,
                                                           int ld, int S, const int* __restrict__ bx0,
                                                           Acc* __restrict__ ws, int nbuf,
@@ -1204,11 +1206,13 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     const int R = S + kBYW - 1;
     Acc* leaves = sm + kBYW * kBYSR;  // parity 1
     constexpr int kRowsPerLane = (kBYMaxS + kBYW - 1 + 31) / 32;  // 9
+    static_assert(NT == kThreadsBY || (NT == kThreadsBYP && V == 5), "576 threads: variant 5 only");
+    const bool act = NT == kThreadsBY || warp < kWarpsBY;  // the warps that own columns
     if (V == 5 && stage != nullptr) {
         // levels 1-2 read the staged columns directly (no leaf tile)
         const unsigned char* __restrict__ sb =
             stage + (size_t)(img_i - img0) * simg + (q < 2 ? st_t : st_p) + s0;
-        if (pmD) {  // u16 pair mode: one tile of words [0, D), S == D
+        if (NT == kThreadsBY && pmD) {  // u16 pair mode: one tile of words [0, D), S == D
             by_level12_staged_pair<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0, pmD);
             __syncthreads();
             if (S == kBYMaxS) {
@@ -1226,13 +1230,17 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
             else by_level5_store_pair<Acc>(sm, warp, lane, dcol0, ld, pmD, H);
             return;
         }
-        by_level12_staged<Acc>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
+        by_level12_staged<Acc, NT / 8>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
         __syncthreads();
         by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
-                           min(S, H - s0));
+                           min(S, H - s0), act);
         return;
     }
-    if (stage != nullptr) {
+    if (!act) {
+        // warps 16.. of a 576-thread CTA: no leaves to load (the q < 2 path
+        // has one barrier)
+        if (q < 2 && stage == nullptr) __syncthreads();
+    } else if (stage != nullptr) {
         // staged u8 columns (k_stage_t/p): 4 leaves per aligned 4-byte load,
         // one 16-byte shared store (lanes contiguous: conflict-free)
         const unsigned char* __restrict__ sb =
@@ -1324,10 +1332,10 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     }
     __syncthreads();
     if constexpr (V >= 4) {  // (V = 5 without staging lands here)
-        by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
+        by_level12<Acc, NT / 8>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
         by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
-                           min(S, H - s0));
+                           min(S, H - s0), act);
         return;
     } else if constexpr (V == 3) {
         by_level12<Acc>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
@@ -1368,12 +1376,8 @@ __global__ void __launch_bounds__(kThreadsBY, 2) k1_by32(const In* __restrict__ 
     }
 }
 
-// K1P of the u16 pair mode on 576 threads: 8 column groups x 72 threads
-// take the 71 level-2 row chunks of a 256-word tile in one round (with 512
-// threads, 7 of each group's 64 threads ran a second item that the whole
-// CTA then waited for); levels 3-5 run on warps 0-15 as in k1_by32.
-// 56 registers keep two CTAs per SM.
-constexpr int kThreadsBYP = 576;
+// K1P of the u16 pair mode on 576 threads (kThreadsBYP): levels 3-5 run on
+// warps 0-15 as in k1_by32.
 template <class Acc>
 __global__ void __launch_bounds__(kThreadsBYP, 2) k1_by32_pair(QuadSet qs, int W, int H, int ld, int S,
                                                                 const int* __restrict__ bx0, Acc* __restrict__ ws,
@@ -1995,10 +1999,13 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                     launched = true;
                 }
             }
+            // variant 5 outside the pair mode: 576 threads (FHT_K1P_576=0: 512)
+            const bool t576 = !launched && g.k1p_variant == 5 && g.k1p_576 && !(stage && g.pm_D);
+            if (t576) kb = k1_by32<In, Acc, 5, kThreadsBYP>;
             if (!launched) {
                 allow_smem(reinterpret_cast<const void*>(kb));
                 dim3 gb(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nby, nslots);
-                launch_k(g.pdl, kb, gb, dim3(kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w,
+                launch_k(g.pdl, kb, gb, dim3(t576 ? kThreadsBYP : kThreadsBY), sm_by, st, reinterpret_cast<const In*>(g.img), g.img_w,
                          g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf,
                          stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, stage ? g.pm_D : 0);
             }

@@ -120,6 +120,7 @@ struct GroupLaunch {
     // K1/K1P/K2 run one row tile of pm_D words, K2's root step widens to 32 bits
     int pm_D;
     int k1p_pair576;  // pair mode: K1P on 576 threads (one round of level-1/2 items)
+    int k1p_576;      // K1P variant 5 outside the pair mode on 576 threads (same reason)
     unsigned char* stage;
     long long stage_pitch, stage_img;
     long long stage_t, stage_p;  // byte offsets inside an image's stage (-1: not staged)

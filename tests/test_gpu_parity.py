@@ -154,6 +154,25 @@ def test_kernel_variants_bit_exact(monkeypatch, k1p, k2, pairs, bulk, stage):
         np.testing.assert_array_equal(out[k][0], ref[k])
 
 
+@pytest.mark.parametrize("k576", [0, 1])
+@pytest.mark.parametrize("ind,acc", [("u8", "i32"), ("i32", "i32"), ("f32", "f32")])
+def test_k1p_thread_counts(monkeypatch, k576, ind, acc):
+    """K1P variant 5 on 576 threads (one round of level-1/2 items; warps 16-17
+    only in those levels) and on 512, unstaged, with full and partial row tiles."""
+    monkeypatch.setenv("FHT_K1P_576", str(k576))
+    monkeypatch.setenv("FHT_K1_STAGE", "0")
+    rng = np.random.default_rng(7 + k576)
+    for strategy, (h, w) in [(1, (600, 333)), (0, (257, 96))]:
+        if ind == "f32":
+            img = rng.standard_normal((h, w)).astype(np.float32)
+        else:
+            img = rng.integers(-100 if ind == "i32" else 0, 256, (h, w)).astype(np.uint8 if ind == "u8" else np.int32)
+        out, _ = run_plan(img, ind, acc, strategy)
+        ref, _ = oracle.fht2d_quadrants(img, strategy, dtype=np.float32 if ind == "f32" else np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][0], ref[k], err_msg=f"{h}x{w} s{strategy} {k}")
+
+
 # --------------------------------------------------- the five configs
 def _cfg_plan(cfg, count=None):
     c = workloads.CONFIGS[cfg]
