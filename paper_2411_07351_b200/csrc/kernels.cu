@@ -1466,14 +1466,18 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
 // Issue the window copies of one K2 tile (all warps; warp per window).  The
 // warp's window records are fetched with one load per lane up front and
 // broadcast with shuffles, so no descriptor load sits on the issue path.
+// srec != 0: the tile's records were copied to shared memory (k2_pair_pipe,
+// which issues the same tile's windows once per slot), each warp's own
+// entries only -- a shared load instead of a global one per slot.
 template <class Acc>
 __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileDev& tile, const Acc* __restrict__ in,
                                               uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
-                                              int lane, uint32_t bar) {
+                                              int lane, uint32_t bar, uint32_t srec = 0u) {
     constexpr int kW = kThreads2 / 32;
     for (int base = 0; base < tile.load_cnt; base += 32 * kW) {
         const int mine = base + warp + kW * lane;
-        const int4 rec = mine < tile.load_cnt ? ps.loads[tile.load_beg + mine] : make_int4(0, 0, 0, 0);
+        const int4 rec = mine < tile.load_cnt ? (srec ? lds4u(srec + 16u * mine) : ps.loads[tile.load_beg + mine])
+                                              : make_int4(0, 0, 0, 0);
         const int cnt = min(32, (tile.load_cnt - base - warp + kW - 1) / kW);
         for (int j = 0; j < cnt; ++j) {
             int4 w;
@@ -1824,8 +1828,14 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
     const int xs0 = (lane & 15) < nc ? ps.stores[tile.store_beg + (lane & 15)].x : 0;
     const int xs1 = (lane & 15) < nc ? ps.stores1[tile.store_beg + (lane & 15)].x : 0;
     const int rows = min(S, pmD - s0), rows_hi = max(0, min(rows, H - pmD - s0));
+    // the window records, after the step offsets: each warp copies the
+    // entries it will issue (so a __syncwarp orders them)
+    const uint32_t srec = smem_u32(ssteps + 64);
+    for (int mine = warp + kWarps * lane; mine < tile.load_cnt; mine += 32 * kWarps)
+        sts4u(srec + 16u * mine, ps.loads[tile.load_beg + mine]);
+    __syncwarp();
     grid_dep_wait();
-    issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u);
+    issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
     cp_async_commit();
     for (int it = 0;; ++it) {
         const int p = it & 1;
@@ -1834,7 +1844,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
         const int next = slot + static_cast<int>(gridDim.z);
         if (next < nslots) {
             issue_windows<Acc>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H, ld,
-                               warp, lane, 0u);
+                               warp, lane, 0u, srec);
             cp_async_commit();
         }
         const int4* ops = sbops + (p ? 2 * nops : 0);
@@ -2042,7 +2052,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             (void)max_nc;
             if (g.pm_D && final_pass && ps.pairs && ps.pipe_delta > 0 && !g.k2_bulk && g.out.layout == 0 &&
                 ps.tile_nc_max <= 16) {
-                const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops);
+                const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops) +
+                                   static_cast<size_t>(ps.pipe_loads) * sizeof(int4);  // + the window records
                 auto kp = k2_pair_pipe<Out>;
                 allow_smem(reinterpret_cast<const void*>(kp));
                 const int rt = (g.pm_D + ps.S - 1) / ps.S;
