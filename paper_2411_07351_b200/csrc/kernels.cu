@@ -834,22 +834,22 @@ __global__ void __launch_bounds__(256) k_stage_u8(const unsigned char* __restric
                                  __byte_perm(t1, t3, 0x7632)};
         const long long y = r0 + 4 * j;
         if (y < pitch_t) {
+            unsigned char* __restrict__ tp = dst + off_t + (size_t)(c0 + 4 * i) * pitch_t + y;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int x = c0 + 4 * i + m;
-                if (x < w) *reinterpret_cast<uint32_t*>(dst + off_t + (size_t)x * pitch_t + y) = col[m];
-            }
+            for (int m = 0; m < 4; ++m, tp += pitch_t)
+                if (c0 + 4 * i + m < w) *reinterpret_cast<uint32_t*>(tp) = col[m];
         }
     }
     if (want_p) {  // word j of P row r = r0 + rr: columns c0 + 4j .. + 3
-        const int j = threadIdx.x & 15;
+        const int j = threadIdx.x & 15, rr0 = threadIdx.x >> 4;
         const long long y = c0 + 4 * j;
+        if (y < pitch_p) {
+            unsigned char* __restrict__ pp = dst + off_p + (size_t)(r0 + rr0) * pitch_p + y;
+            const size_t pstep = 16 * (size_t)pitch_p;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int rr = (threadIdx.x >> 4) + 16 * k, r = r0 + rr;
-            if (r < h && y < pitch_p)
-                *reinterpret_cast<uint32_t*>(dst + off_p + (size_t)r * pitch_p + y) =
-                    *reinterpret_cast<const uint32_t*>(&tile[rr][4 * j]);
+            for (int k = 0; k < 4; ++k, pp += pstep)
+                if (r0 + rr0 + 16 * k < h)
+                    *reinterpret_cast<uint32_t*>(pp) = *reinterpret_cast<const uint32_t*>(&tile[rr0 + 16 * k][4 * j]);
         }
     }
 }
