@@ -6,8 +6,9 @@ Contract:
 
 One step = one pass of the hot path over one batch of the workload (default
 config c4: 256 binary 509x509 edge maps, all four quadrants, u8 -> int32).
-Each rank processes its own 256-image shard (weak scaling; no collective on
-the data path).  `value` is whole-job FHT Gsums/s (BASELINE.json metric:
+On N GPUs the 256-image batch is sharded 256/N per rank (strong scaling, the
+BASELINE.json c4 configuration; --scaling weak gives every rank a whole
+batch); no collective on the data path.  `value` is whole-job FHT Gsums/s (BASELINE.json metric:
 Q * images * n^2 * ceil(log2 n) nominal adds / s) with inputs resident in HBM;
 `e2e` is the same metric through the C-ABI host-buffer call
 (fht_execute_host: H2D of the inputs + transform + D2H of every Hough image).
@@ -53,7 +54,22 @@ def parse():
                     help="replay one captured CUDA graph per step instead of launching through the API "
                          "(measured: no gain; programmatic dependent launch already hides the gaps)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="batch configs on N GPUs: strong = BASELINE's one batch sharded 1/N per GPU "
+                         "(images/s = batch / max t); weak = a whole batch per GPU")
     return ap.parse_args()
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def hbm_peak():
@@ -178,9 +194,43 @@ def cpu_baseline(cfg: str, strategy: int, seconds: float, threads: int | None = 
     dt = time.perf_counter() - t0
     sums = len(quads) * done * c.n * c.n * int(np.ceil(np.log2(c.n)))
     used = min(threads, per * len(quads))  # work items are (image, quadrant) pairs
-    return {"value": sums / dt / 1e9, "unit": "Gsums/s", "cores": used, "kind": kind,
+    return {"value": sums / dt / 1e9, "unit": "Gsums/s", "cores": used, "kind": kind, "cpu_model": cpu_model(),
             "sample": f"{done} image(s) of {cfg} ({c.n}x{c.n}, {len(quads)} quadrant(s)){proxy}, "
                       f"{dt:.2f} s, (image, quadrant) items over {used} host thread(s)"}
+
+
+def cpu_single_thread(cfg: str, strategy: int, seconds: float):
+    """The reference as it runs: one host thread, fht2d_quadrants (or fht2d for
+    a one-quadrant config) image after image (quadrants.cpp:23-41,
+    transform.cpp:62-85).  Large images: whole (image, quadrant) transforms
+    until `seconds` have passed (at least one), counted per quadrant."""
+    import oracle
+
+    c = workloads.CONFIGS[cfg]
+    kind = "reference" if oracle.ref_available() else "port"
+    fn = oracle.ref_batch_quadrants_u8 if kind == "reference" else oracle.batch_quadrants_u8_port
+    if c.dtype == "u8":
+        img = workloads.make_images(cfg, 1)
+        proxy = ""
+    else:
+        img = np.random.default_rng(0).integers(0, 256, (1, c.n, c.n), dtype=np.uint8)
+        proxy = " (int64 proxy: reference has no float path)"
+    # one quadrant per call keeps a sample of the largest image bounded; every
+    # quadrant of a square image costs the same
+    full = sum(1 << workloads.ALL_Q.index(q) for q in c.quadrants)
+    mask = full if c.n * c.n * len(c.quadrants) <= (4 << 20) else 1 << workloads.ALL_Q.index(c.quadrants[0])
+    nq = bin(mask).count("1")
+    t0 = time.perf_counter()
+    calls = 0
+    while True:
+        fn(img, strategy, threads=1, mask=mask)
+        calls += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    sums = nq * calls * c.n * c.n * int(np.ceil(np.log2(c.n)))
+    return {"value": sums / dt / 1e9, "unit": "Gsums/s", "cores": 1, "kind": kind,
+            "sample": f"{calls} x {nq} quadrant(s) of one {c.n}x{c.n} image of {cfg}{proxy}, {dt:.2f} s, 1 thread"}
 
 
 def run_reference(args):
@@ -207,9 +257,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "FHT Gsums/s", "value": value, "unit": "Gsums/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "scaling": args.scaling if c.batch > 1 else "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.config, "description": c.description, "strategy": args.strategy},
         "cpu_baseline": {"value": value, "unit": "Gsums/s", "cores": sample["cores"], "kind": sample["kind"],
+                         "cpu_model": sample.get("cpu_model"),
                          "sample": sample["sample"]},
         "e2e": {"value": value, "unit": "Gsums/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -238,34 +289,37 @@ def run_ours(args):
     strategy = 0 if args.strategy == "simple" else 1
 
     root_split = None
-    if c.batch == 1 and ws > len(c.quadrants):
-        # one large image on more ranks than quadrants: two ranks per quadrant,
-        # each computes one child subtree of the root, they swap half of their
-        # child columns (one NCCL send/recv pair) and each merges half the root
-        pair = rank // 2
-        my_q = [c.quadrants[pair]] if pair < len(c.quadrants) else []
-        root_split = (rank % 2, rank ^ 1) if my_q and (rank ^ 1) < ws else None
-        if my_q and root_split is None:
-            my_q = list(my_q)  # unpaired last rank: whole quadrant alone
+    n_local = c.batch  # images this rank transforms per step
+    if c.batch == 1 and ws > 1:
+        # one large image: its quadrants over the ranks; with more ranks than
+        # quadrants, pairs of ranks split a quadrant's root (each computes one
+        # child subtree, the exchange fused into its last pass, each merges
+        # half the root) -- every quadrant owned (shard.image_assignment)
+        a = shard.image_assignment(ws, rank, c.quadrants)
+        my_q = list(a.quadrants)
+        root_split = (a.side, a.peer) if a.side is not None else None
         imgs = workloads.make_images(args.config, 1)
         scaling = "strong"
         sums_per_step = workloads.nominal_sums(args.config)
-    elif c.batch == 1 and ws > 1:
-        # one large image: split its quadrants over the ranks (strong scaling)
-        my_q = shard.quadrant_shard(ws, rank, c.quadrants)
-        imgs = workloads.make_images(args.config, 1)
+    elif ws > 1 and args.scaling == "strong":
+        # BASELINE's batch sharded across the GPUs: 256 / N images per rank,
+        # images/s = 256 / (max over ranks of the step time); no collective
+        sh = shard.batch_shard(c.batch, ws, rank)
+        n_local = sh.count
+        my_q = list(c.quadrants) if n_local > 0 else []
+        imgs = workloads.make_images(args.config, max(1, n_local), offset=sh.start)
         scaling = "strong"
         sums_per_step = workloads.nominal_sums(args.config)
     else:
-        # a batch per rank, no collective on the data path (weak scaling)
+        # a whole batch per rank, no collective on the data path (weak scaling)
         my_q = list(c.quadrants)
         imgs = workloads.make_images(args.config, c.batch, offset=rank * c.batch)
         scaling = "weak"
         sums_per_step = workloads.nominal_sums(args.config) * ws
-    if not my_q:  # more ranks than quadrants: this rank idles but joins the timing
+    if not my_q:  # more ranks than work: this rank idles but joins the timing
         my_q = None
     plan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=my_q or [c.quadrants[0]],
-                    batch=c.batch, device=local)
+                    batch=max(1, n_local), device=local)
     x = torch.from_numpy(imgs).to(dev)
     out = plan.alloc_outputs()
     wsbuf = plan.workspace()
@@ -386,7 +440,7 @@ def run_ours(args):
     # are this design's overhead traffic, reported on their own
     total_bytes = sum(b for kd, b in zip(kinds, launch_bytes) if kd != 5)
     staging_bytes = sum(b for kd, b in zip(kinds, launch_bytes) if kd == 5)
-    step_gbs = total_bytes / (sum(med) * 1e-3) / 1e9
+    step_gbs = total_bytes / (ms_per_step * 1e-3) / 1e9  # over the event-timed step, not the serialised launches
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": int(dom_bytes), "avg_launch_ms": round(dom_ms, 5),
@@ -401,7 +455,7 @@ def run_ours(args):
     # K = ceil(log2 n) passes).  The fused passes here are shared-memory bound
     # (low per-pass HBM fraction) yet beat that floor by this factor.
     levels = int(np.ceil(np.log2(c.n)))
-    imgs_here = c.batch if scaling == "weak" else 1
+    imgs_here = n_local
     nq_here = len(my_q) if my_q else 0
     unfused = nq_here * imgs_here * c.n * c.n * (ESZ[c.dtype] + ESZ[c.acc] + 2 * ESZ[c.acc] * (levels - 1))
     floor_ms = unfused / (peak * 1e9) * 1e3
@@ -419,6 +473,11 @@ def run_ours(args):
             lsu = pj.get("lsu_issue", {}).get(args.config, {}).get(names[dom])
             if lsu:
                 roofline["lsu_pipe_frac_ncu"], roofline["issue_frac_ncu"] = lsu
+                # the kernel's floor if its LSU data pipe (shared-memory and
+                # global wavefronts, one per SM clock) ran at 100 %, and the
+                # HBM fraction that floor would give: why frac < 1
+                roofline["lsu_floor_ms"] = round(lsu[0] * dom_ms, 4)
+                roofline["frac_at_lsu_floor"] = round(achieved / lsu[0] / peak, 4)
         except Exception:
             pass
 
@@ -449,6 +508,35 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, strategy, args.cpu_seconds)
+        cpu["single_thread"] = cpu_single_thread(args.config, strategy, max(1.0, args.cpu_seconds / 2))
+
+    weak = None
+    if ws > 1 and scaling == "strong" and c.batch > 1 and my_q is not None and not args.no_e2e:
+        # extra key: the weak-scaling figure (a whole batch per GPU) beside the
+        # strong-scaling headline
+        wplan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=my_q, batch=c.batch,
+                         device=local)
+        wx = torch.from_numpy(workloads.make_images(args.config, c.batch, offset=rank * c.batch)).to(dev)
+        wout = wplan.alloc_outputs()
+        for _ in range(2):
+            wplan(wx, out=wout)
+        nw = max(3, min(args.steps, 10))
+        torch.cuda.synchronize()
+        dist.barrier()
+        ws_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nw)]
+        for s0, e0 in ws_ev:
+            flush.fill_(1)
+            s0.record(stream)
+            wplan(wx, out=wout)
+            e0.record(stream)
+        torch.cuda.synchronize()
+        wt = torch.tensor([sum(a.elapsed_time(b) for a, b in ws_ev) / nw], dtype=torch.float64, device=dev)
+        dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wms = float(wt.item())
+        weak = {"value": round(workloads.nominal_sums(args.config) * ws / (wms * 1e-3) / 1e9, 3),
+                "unit": "Gsums/s", "ms_per_step": round(wms, 4), "images_per_s": round(c.batch * ws / (wms * 1e-3), 1),
+                "images_per_gpu": c.batch}
+        del wplan, wx, wout
 
     if rank == 0:
         line = {
@@ -457,13 +545,16 @@ def run_ours(args):
             "scaling": scaling, "vs_baseline": None, "dtype": c.acc,
             "data": "synthetic (seeded, BASELINE.json config shapes/distributions)",
             "config": {"workload": args.config, "description": c.description, "n": c.n,
-                       "images_per_gpu": c.batch, "quadrants": len(c.quadrants), "strategy": args.strategy,
+                       "images_per_gpu": n_local, "quadrants": len(c.quadrants), "strategy": args.strategy,
                        "cuda_graph": graph is not None,
                        "in_dtype": c.dtype, "acc_dtype": c.acc,
-                       "parallelism": (("root-split x2 per quadrant" if ws > len(c.quadrants) else f"quadrant-split x{ws}")
-                                       if scaling == "strong" else f"batch-shard x{ws}"),
+                       "parallelism": (f"batch-shard x{ws} ({c.batch}/{ws} images per GPU)" if c.batch > 1 and scaling == "strong"
+                                       else f"batch per GPU x{ws}" if c.batch > 1
+                                       else "root-split x2 per quadrant" if ws > len(c.quadrants)
+                                       else f"quadrant-split x{ws}"),
                        "l2": "flushed between timed steps (512 MiB write, untimed)"},
-            "images_per_s": round((c.batch * ws if scaling == "weak" else 1) / (ms_per_step * 1e-3), 1),
+            "images_per_s": round((c.batch * ws if scaling == "weak" else c.batch) / (ms_per_step * 1e-3), 1),
+            "weak_scaling": weak,
             "hbm_gbs_step": round(step_gbs, 1),
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -67,8 +67,14 @@ typedef struct fht_plan_s* fht_plan_t;
  *   (u8|i32, i32, i32)  (u8|i32|i64, i32, i64)  (u8|i32|i64, i64, i64)
  *   (f32|u8, f32, f32)
  * An i32 accumulator for u8 input requires W*255 < 2^31 (else
- * FHT_ERR_OVERFLOW).  `batch` images are processed per execute.  The plan is
- * immutable after creation and may be shared by host threads.
+ * FHT_ERR_OVERFLOW).  `batch` images are processed per execute.  The plan's
+ * tables are immutable after creation, and host threads may execute one plan
+ * concurrently, each on its own stream with its own workspace and outputs
+ * (the reference's transforms are safe to call concurrently):
+ * the plan-owned auxiliary stream's fork/join events are recorded and waited
+ * under a per-plan lock, so every call's kernels are ordered after its own
+ * stream's prior work.  fht_execute_host serialises on a per-plan lock (it
+ * uses plan-owned device staging buffers).
  * Replaces the per-call scratch set-up of fht::fht2d_counted
  * (transform.cpp:62-78). */
 int fht_plan_create(int width, int height, int strategy, int in_dtype, int acc_dtype, int out_dtype,
@@ -212,6 +218,14 @@ int fht_count_additions_tree(int w, int h, int strategy, uint64_t* result); /* o
  * Returns FHT_ERR_INVALID if `len` is too small (then *needed holds the size). */
 int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_levels, int tile_width, char* buf,
                       size_t len, size_t* needed);
+
+/* The plans behind fht_fht2d_counted_i64 / fht_fht2d_quadrants_i64 are cached
+ * per (size, strategy, accumulator, quadrants, device), least recently used
+ * first out, at most FHT_PLAN_CACHE (environment, default 8).  Release them
+ * all (e.g. before cudaDeviceReset); *released (may be NULL) = how many.
+ * Plans a concurrent call is still using are freed when it returns. */
+int fht_plan_cache_clear(size_t* released);
+size_t fht_plan_cache_size(void);
 
 /* Message of the last failed call on this thread ("" if none). */
 const char* fht_last_error(void);

@@ -127,8 +127,9 @@ def ref():
         lib.ref_count_additions_tree.restype = ctypes.c_uint64
         lib.ref_batch_quadrants_u8.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_i64p, cp, ctypes.c_int]
+        lib.ref_rotate.argtypes = [_c_i64p, ctypes.c_int, ctypes.c_int, _c_i64p, cp, ctypes.c_int]
         for f in ("ref_fht2d_counted", "ref_fht2d_quadrants", "ref_slow_hough", "ref_fht2d_pattern",
-                  "ref_batch_quadrants_u8"):
+                  "ref_batch_quadrants_u8", "ref_rotate"):
             getattr(lib, f).restype = ctypes.c_int
     return _ref
 
@@ -266,6 +267,16 @@ def ref_fht2d_quadrants(img: np.ndarray, strategy: int = TWEAKED):
                                    *[_ptr(o, ctypes.c_int64) for o in outs], ctypes.byref(adds), e, 256)
     _raise(rc, e.value.decode())
     return dict(zip(QUADRANTS, outs)), int(adds.value)
+
+
+def ref_rotate(v, r: int) -> np.ndarray:
+    """The reference's own fht::rotate (transform.cpp:8-14)."""
+    a = np.ascontiguousarray(v, dtype=np.int64).reshape(-1)
+    out = np.empty_like(a)
+    e = _err()
+    _raise(ref().ref_rotate(_ptr(a, ctypes.c_int64), a.size, int(r), _ptr(out, ctypes.c_int64), e, 256),
+           e.value.decode())
+    return out
 
 
 def ref_slow_hough(img: np.ndarray, strategy: int = TWEAKED) -> np.ndarray:

@@ -127,7 +127,13 @@ int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int stra
         std::vector<int> quads;
         for (int q = 0; q < 4; ++q)
             if (quadrant_mask & (1 << q)) quads.push_back(q);
-        const int n_items = n_img * static_cast<int>(quads.size());
+        // whole images per work item once there are enough of them: then
+        // each item is exactly the reference's own fht2d_quadrants (one
+        // transpose per image, quadrants.cpp:23-41); fewer images than
+        // threads: (image, quadrant) items, so one image's quadrants run in
+        // parallel
+        const bool per_image = quadrant_mask == 15 && n_img >= std::max(1, threads);
+        const int n_items = per_image ? n_img : n_img * static_cast<int>(quads.size());
         std::atomic<int> next{0};
         std::atomic<int> failed{0};
         std::string first_error;
@@ -135,8 +141,22 @@ int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int stra
             for (;;) {
                 const int k = next.fetch_add(1);
                 if (k >= n_items || failed.load()) return;
-                const int i = k / static_cast<int>(quads.size()), q = quads[static_cast<std::size_t>(k) % quads.size()];
                 try {
+                    if (per_image) {
+                        std::vector<int64_t> v(cells);
+                        const uint8_t* src = img + static_cast<std::size_t>(k) * cells;
+                        for (std::size_t c = 0; c < cells; ++c) v[c] = src[c];
+                        fht::QuadrantSet qs = fht::fht2d_quadrants(fht::Image(w, h, std::move(v)), strat(strategy));
+                        if (out) {
+                            int64_t* o = out + static_cast<std::size_t>(k) * 4 * cells;
+                            copy_out(qs.horiz_pos, o);
+                            copy_out(qs.horiz_neg, o + cells);
+                            copy_out(qs.vert_pos, o + 2 * cells);
+                            copy_out(qs.vert_neg, o + 3 * cells);
+                        }
+                        continue;
+                    }
+                    const int i = k / static_cast<int>(quads.size()), q = quads[static_cast<std::size_t>(k) % quads.size()];
                     std::vector<int64_t> v(cells);
                     const uint8_t* src = img + static_cast<std::size_t>(i) * cells;
                     for (std::size_t c = 0; c < cells; ++c) v[c] = src[c];
@@ -160,6 +180,14 @@ int ref_batch_quadrants_u8(const uint8_t* img, int n_img, int w, int h, int stra
         worker();
         for (auto& t : pool) t.join();
         if (failed.load()) throw std::runtime_error(first_error);
+    });
+}
+
+// transform.cpp:8-14: u(i) = v((i + r) mod h)
+int ref_rotate(const int64_t* v, int h, int r, int64_t* out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const std::vector<fht::Accum> u = fht::rotate(std::span<const fht::Accum>(v, static_cast<std::size_t>(h)), r);
+        std::memcpy(out, u.data(), u.size() * sizeof(int64_t));
     });
 }
 

@@ -56,6 +56,8 @@ SIGNATURES = {
     "fht_round_half_up_ratio": (_i, [_i64, _i64, _pi64]),
     "fht_count_additions_tree": (_i, [_i, _i, _i, _pu64]),
     "fht_schedule_json": (_i, [_i, _i, _i, _i, _i, _i, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "fht_plan_cache_clear": (_i, [ctypes.POINTER(ctypes.c_size_t)]),
+    "fht_plan_cache_size": (ctypes.c_size_t, []),
     "fht_last_error": (ctypes.c_char_p, []),
     "fht_version": (ctypes.c_char_p, []),
 }

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -153,6 +154,7 @@ struct fht_plan_s {
     void* st_ws = nullptr;
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::mutex fork_mu;  // serialises each ev_fork/ev_join record + wait pair (kernels.cu launch_typed)
     cudaStream_t hst[kHostStreams] = {};  // execute_host pipeline
     cudaEvent_t hev[kHostStreams] = {};
     cudaEvent_t hev_start = nullptr;
@@ -665,6 +667,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.aux_stream = env_int("FHT_K1_OVERLAP", 1, 0, 1) ? p->aux : nullptr;
             L.ev_fork = p->ev_fork;
             L.ev_join = p->ev_join;
+            L.fork_mu = &p->fork_mu;
             L.shapes = g.dt.shapes;
             L.step_offs = g.dt.step_offs;
             L.k1_ops = g.dt.k1_ops;
@@ -779,18 +782,66 @@ void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok
     if (ok_i32) *ok_i32 = prod < (static_cast<unsigned __int128>(1) << 31);
 }
 
-// Per-device cache of plans used by the int64 reference entry points.
-std::mutex g_cache_mu;
-std::map<std::tuple<int, int, int, int, int, int>, std::unique_ptr<fht_plan_s>> g_cache;
+// Per-device cache of plans used by the int64 reference entry points:
+// least-recently-used, at most FHT_PLAN_CACHE (default 8) plans, so a process
+// that transforms many image sizes does not keep a stream, events and device
+// tables for each forever.  Entries are shared_ptrs: a plan evicted while
+// another thread executes it lives until that call returns.  The cache object
+// is deliberately never destroyed (a static destructor would run after the
+// CUDA runtime's teardown); fht_plan_cache_clear releases it explicitly.
+using CacheKey = std::tuple<int, int, int, int, int, int>;
+struct PlanCache {
+    std::mutex mu;
+    std::list<std::pair<CacheKey, std::shared_ptr<fht_plan_s>>> lru;  // front = most recent
+};
+PlanCache& plan_cache() {
+    static PlanCache* c = new PlanCache;
+    return *c;
+}
 
-fht_plan_s* cached_plan(int w, int h, int strategy, int acc, int mask, int device) {
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto key = std::make_tuple(w, h, strategy, acc, mask, device);
-    auto it = g_cache.find(key);
-    if (it != g_cache.end()) return it->second.get();
-    fht_plan_s* p = create_plan(w, h, strategy, FHT_I64, acc, FHT_I64, mask, 1, FHT_LAYOUT_REFERENCE, device);
-    g_cache.emplace(key, std::unique_ptr<fht_plan_s>(p));
+std::shared_ptr<fht_plan_s> cached_plan(int w, int h, int strategy, int acc, int mask, int device) {
+    PlanCache& c = plan_cache();
+    const auto key = std::make_tuple(w, h, strategy, acc, mask, device);
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
+            if (it->first == key) {
+                c.lru.splice(c.lru.begin(), c.lru, it);
+                return it->second;
+            }
+    }
+    // build outside the lock (plan creation uploads tables); a racing thread
+    // may build the same plan, the first insert wins
+    std::shared_ptr<fht_plan_s> p(create_plan(w, h, strategy, FHT_I64, acc, FHT_I64, mask, 1, FHT_LAYOUT_REFERENCE, device));
+    std::vector<std::shared_ptr<fht_plan_s>> evicted;  // destroyed after the lock is released
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto& e : c.lru)
+            if (e.first == key) return e.second;
+        c.lru.emplace_front(key, p);
+        const size_t cap = static_cast<size_t>(env_int("FHT_PLAN_CACHE", 8, 1, 1024));
+        while (c.lru.size() > cap) {
+            evicted.push_back(std::move(c.lru.back().second));
+            c.lru.pop_back();
+        }
+    }
     return p;
+}
+
+size_t plan_cache_clear() {
+    PlanCache& c = plan_cache();
+    std::list<std::pair<CacheKey, std::shared_ptr<fht_plan_s>>> gone;
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        gone.swap(c.lru);
+    }
+    return gone.size();
+}
+
+size_t plan_cache_size() {
+    PlanCache& c = plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    return c.lru.size();
 }
 
 void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* const outs[4], uint64_t* adds) {
@@ -818,7 +869,8 @@ void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* 
         int ok32 = 0;
         const int wmax = std::max((mask & 3) ? w : 0, (mask & 12) ? h : 0);
         check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), wmax, &ok32, st);
-        fht_plan_s* p = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev);
+        const std::shared_ptr<fht_plan_s> sp = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev);
+        fht_plan_s* p = sp.get();
         for (int q = 0; q < 4; ++q)
             if (mask & (1 << q)) cuda_check(cudaMallocAsync(&d_out[q], cells * 8, st), "cudaMallocAsync(out)");
         if (p->ws_bytes) cuda_check(cudaMallocAsync(&d_ws, p->ws_bytes, st), "cudaMallocAsync(ws)");
@@ -1267,6 +1319,15 @@ int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_leve
 }
 
 const char* fht_last_error(void) { return g_last_error.c_str(); }
+
+int fht_plan_cache_clear(size_t* released) {
+    return guarded([&] {
+        const size_t n = plan_cache_clear();
+        if (released) *released = n;
+    });
+}
+
+size_t fht_plan_cache_size(void) { return plan_cache_size(); }
 
 const char* fht_version(void) { return "fht_b200 0.1 (sm_100a)"; }
 

@@ -1973,12 +1973,18 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             stage = g.stage;
         }
     }
-    const bool both = (sizeof(Acc) == 4) && g.nby > 0 && g.nblocks > 0 && g.aux_stream && !hook;
+    const bool both = (sizeof(Acc) == 4) && g.nby > 0 && g.nblocks > 0 && g.aux_stream && g.fork_mu && !hook;
     cudaStream_t st1 = both ? g.aux_stream : st;
-    if (both) {
-        cudaEventRecord(g.ev_fork, st);
-        cudaStreamWaitEvent(st1, g.ev_fork, 0);
-    }
+    // cudaStreamWaitEvent binds to the event's most recent record at call
+    // time, so holding the plan's lock across each record + wait pair is all
+    // concurrent callers need (they may then share the aux stream: at worst a
+    // false dependency, never a missing one)
+    auto fork_join = [&](cudaEvent_t ev, cudaStream_t from, cudaStream_t to) {
+        std::lock_guard<std::mutex> lk(*static_cast<std::mutex*>(g.fork_mu));
+        cudaEventRecord(ev, from);
+        cudaStreamWaitEvent(to, ev, 0);
+    };
+    if (both) fork_join(g.ev_fork, st, st1);
     if (g.nblocks > 0) {
         dim3 g1(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nblocks, nslots);
         auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;
@@ -2023,10 +2029,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             if (hook) hook(ctx, 4);
         }
     }
-    if (both) {
-        cudaEventRecord(g.ev_join, st1);
-        cudaStreamWaitEvent(st, g.ev_join, 0);
-    }
+    if (both) fork_join(g.ev_join, st1, st);
     if (g.root_is_block) return launches;
     const long long slot_elems = (long long)g.nbuf * g.W * g.ld;
     for (int p = 0; p < g.npasses; ++p) {

@@ -91,6 +91,10 @@ struct GroupLaunch {
     const int* by_x0;
     cudaStream_t aux_stream;  // plan-owned stream for the concurrent generic-block K1 (may be null)
     cudaEvent_t ev_fork, ev_join;
+    // held around each event record + stream wait pair: a plan (and so its
+    // aux stream and events) may be executed by several host threads at
+    // once, and a wait must see the record of its own call (std::mutex*)
+    void* fork_mu;
     int k1p_variant;    // 5 (default): 4, with levels 1-2 reading the staged u8 columns directly
                         // (no leaf tile) when the input is staged; 4: levels 1-2 in registers,
                         // 3-5 rows interleaved over lanes, the root stored from registers;

@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import json
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -106,6 +107,19 @@ def count_additions_tree(w: int, h: int, strategy=SplitStrategy.Tweaked) -> int:
     r = ctypes.c_uint64()
     check(lib().fht_count_additions_tree(w, h, _strategy(strategy), ctypes.byref(r)))
     return int(r.value)
+
+
+def rotate(v, r: int) -> np.ndarray:
+    """fht::rotate (transform.cpp:8-14; SPEC.md:74-81): u(i) = v((i + r) mod h),
+    r in [0, h) or InvalidArgument.  A host helper kept for API compatibility:
+    the device merge applies the same circular shift inline (its window reads
+    b[(s + r) mod h], transform.cpp:53-55)."""
+    a = np.asarray(v, dtype=np.int64).reshape(-1)
+    h = a.size
+    r = int(r)
+    if r < 0 or r >= h:
+        raise InvalidArgument("rotate: shift must lie in [0, h)")
+    return np.concatenate((a[r:], a[:r]))
 
 
 def schedule(W: int, H: int, strategy=SplitStrategy.Tweaked, block_width: int = 32, pass_levels: int = 5,
@@ -267,7 +281,8 @@ class Plan:
         self.workspace_bytes = int(lib().fht_workspace_bytes(h))
         self.additions = int(lib().fht_additions(h))
         self.launches = int(lib().fht_launches_per_execute(h))
-        self._ws = None
+        self._ws = {}
+        self._ws_lock = threading.Lock()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -304,12 +319,23 @@ class Plan:
         return {q: torch.empty((self.batch, *self.out_shape(q)), dtype=self._torch_dtype(self.out_dtype), device=dev)
                 for q in self.quadrants}
 
-    def workspace(self):
+    def workspace(self, stream=None):
+        """The device workspace for calls on `stream` (default: the current
+        stream).  One buffer per stream: host threads may share a plan, each
+        on its own stream, without sharing scratch (the reference allocates
+        its scratch per call, transform.cpp:70-76)."""
         import torch
 
-        if self._ws is None and self.workspace_bytes:
-            self._ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=torch.device("cuda", self.device))
-        return self._ws
+        if not self.workspace_bytes:
+            return None
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        key = int(st.cuda_stream)
+        with self._ws_lock:
+            ws = self._ws.get(key)
+            if ws is None:
+                ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=torch.device("cuda", self.device))
+                self._ws[key] = ws
+        return ws
 
     def __call__(self, x, out: dict | None = None, stream=None):
         import torch
@@ -325,8 +351,8 @@ class Plan:
         ptrs = (ctypes.c_void_p * 4)()
         for i, q in enumerate(QUADRANTS):
             ptrs[i] = out[q].data_ptr() if q in out else None
-        ws = self.workspace()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ws = self.workspace(st)
         cells = self.width * self.height
         check(lib().fht_execute(self._h, ctypes.c_void_p(x.data_ptr()), cells, ptrs, cells,
                                 ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
@@ -358,7 +384,7 @@ class Plan:
 
 
 __all__ = ["SplitStrategy", "strategy_from_string", "split_width", "split_simple", "split_tweaked",
-           "round_half_up_ratio", "count_additions_tree", "CountedTransform", "QuadrantSet", "fht2d", "Pattern",
+           "round_half_up_ratio", "count_additions_tree", "rotate", "CountedTransform", "QuadrantSet", "fht2d", "Pattern",
            "fht2d_pattern", "pattern_set", "slow_hough", "slow_hough_device",
            "fht2d_counted", "fht2d_quadrants", "check_overflow_budget", "Plan", "QUADRANTS", "InvalidArgument",
            "OverflowBudget", "_lib"]

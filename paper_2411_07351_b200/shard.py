@@ -5,8 +5,8 @@ the data path.
   contiguous, balanced shard of the batch (`batch_shard`).
 * One large image (config c5): the four quadrants are independent -> rank r
   transforms the quadrants assigned to it (`quadrant_shard`).
-* One large image on 8 ranks (c5): two GPUs per quadrant split its root
-  (`root_split_quadrant`); the one exchange is fused into the child
+* One large image on more ranks than quadrants (c5 on 8 GPUs): two GPUs per
+  quadrant split its root (`image_assignment`, `root_split_quadrant`); the one exchange is fused into the child
   transform, whose last pass stores the slopes the peer needs straight into
   the peer's buffer over NVLink (`PeerExchange`, CUDA IPC), NCCL/gloo
   send/recv as the fallback.
@@ -42,10 +42,38 @@ def batch_shard(n_items: int, world: int, rank: int) -> Shard:
 def quadrant_shard(world: int, rank: int, quadrants=QUADRANTS) -> list[str]:
     """Quadrants of one image owned by `rank`: round-robin, so 4 ranks get one
     each, 2 ranks two each; with more ranks than quadrants the extra ranks get
-    none (a root split of one quadrant over two GPUs is future work)."""
+    none (`image_assignment` pairs them up for a root split instead)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("invalid world/rank")
     return [q for i, q in enumerate(quadrants) if i % world == rank]
+
+
+@dataclass(frozen=True)
+class Assignment:
+    """What one rank computes of a single large image: `quadrants` whole, or
+    (when `side` is not None) one child subtree of `quadrants[0]`'s root,
+    paired with rank `peer` (root_split_quadrant)."""
+    quadrants: tuple
+    side: int | None = None
+    peer: int | None = None
+
+
+def image_assignment(world: int, rank: int, quadrants=QUADRANTS) -> Assignment:
+    """Work of `rank` for one image on `world` ranks, every quadrant owned:
+    world <= Q: quadrants round-robin (quadrant_shard).  Q < world: the first
+    world - Q quadrants (at most Q) get two ranks each and are root-split, the
+    rest one rank each; ranks past 2Q idle.  E.g. Q = 4, world = 6: quadrants
+    0 and 1 on ranks (0, 1) and (2, 3), quadrants 2 and 3 on ranks 4 and 5."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid world/rank")
+    nq = len(quadrants)
+    if world <= nq:
+        return Assignment(tuple(quadrant_shard(world, rank, quadrants)))
+    split = min(nq, world - nq)  # quadrants that get a pair of ranks
+    if rank < 2 * split:
+        return Assignment((quadrants[rank // 2],), rank % 2, rank ^ 1)
+    k = split + (rank - 2 * split)  # a single-rank quadrant, or idle
+    return Assignment((quadrants[k],) if k < nq else ())
 
 
 def gather_to_root(tensor, group=None, dst: int = 0):

@@ -191,6 +191,28 @@ def test_config_c1_bit_exact():
     np.testing.assert_array_equal(out2["horiz_pos"][0], oracle.fht2d(imgs[0], 1, dtype=np.int32)[0])
 
 
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref (the compiled reference) not built")
+def test_configs_c1_c2_against_compiled_reference():
+    """Full-size parity against the reference library itself (not the port):
+    c1 = vert_pos = fht::fht2d(transpose(I)) (transform.cpp:62-89), c2 = the
+    four quadrants of fht::fht2d_quadrants (quadrants.cpp:23-41), int64."""
+    c, imgs, out, _ = _cfg_plan("c1")
+    ref, adds = oracle.ref_fht2d_counted(np.ascontiguousarray(imgs[0].T))
+    np.testing.assert_array_equal(out["vert_pos"][0], ref)
+    assert adds == 9_984_000
+    c, imgs, out, _ = _cfg_plan("c2")
+    ref, adds = oracle.ref_fht2d_quadrants(imgs[0])
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
+    assert adds == 4 * 10_485_760
+    # and the int64 drop-in entry point on the same image
+    tot = []
+    qs = fht.fht2d_quadrants(imgs[0].astype(np.int64), "tweaked", tot)
+    for k in Q:
+        np.testing.assert_array_equal(getattr(qs, k), ref[k])
+    assert tot == [adds]
+
+
 def test_config_c2_bit_exact_and_strategies_coincide():
     c, imgs, out, plan = _cfg_plan("c2")
     ref, adds = oracle.fht2d_quadrants(imgs[0], 1, dtype=np.int32)
@@ -228,6 +250,15 @@ def test_config_c4_batch():
         ref, _ = oracle.fht2d_quadrants(imgs[bi], 1, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][bi], ref[k])
+    if oracle.ref_available():
+        # all 256 images x 4 quadrants against the compiled reference itself
+        # (fht::fht2d_quadrants, quadrants.cpp:23-41, on the host threads)
+        for b0 in range(0, 256, 32):
+            ref = oracle.ref_batch_quadrants_u8(imgs[b0:b0 + 32], 1, threads=oracle.host_threads(),
+                                                want_output=True)
+            for qi, k in enumerate(Q):
+                got = out[k][b0:b0 + 32].reshape(32, -1)
+                assert np.array_equal(got, ref[:, qi]), (b0, k)
     # every image: mass conservation per slope, a size-independent property
     mass = imgs.reshape(256, -1).sum(axis=1).astype(np.int64)
     for k in Q:
@@ -238,7 +269,7 @@ def test_config_c4_batch():
 def test_config_c5_float32():
     c, imgs, out, plan = _cfg_plan("c5")
     img = imgs[0]
-    for k in ("horiz_pos", "vert_neg"):  # two quadrants against the full oracle (~10 s each)
+    for k in Q:  # all four quadrants against the full fp32 and fp64 trees (~10 s each)
         _float_check(img, out[k][0], k)
     tot = float(img.astype(np.float64).sum())
     for k in Q:  # all four: mass conservation within fp32 rounding

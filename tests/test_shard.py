@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2411_07351_b200.shard import QUADRANTS, batch_shard, gather_to_root, max_over_ranks, quadrant_shard
+from paper_2411_07351_b200.shard import (QUADRANTS, batch_shard, gather_to_root, image_assignment, max_over_ranks,
+                                         quadrant_shard)
 
 
 def test_batch_shard_covers_exactly_once():
@@ -32,6 +33,29 @@ def test_quadrant_shard():
     assert sum((quadrant_shard(8, r) for r in range(8)), []) == list(QUADRANTS)
     with pytest.raises(ValueError):
         batch_shard(4, 2, 2)
+
+
+@pytest.mark.parametrize("world", range(1, 11))
+def test_image_assignment_owns_every_quadrant(world):
+    """Every quadrant of a single image is computed for any world size: whole
+    by one rank, or root-split by a pair of ranks that name each other."""
+    owners = {q: [] for q in QUADRANTS}
+    for r in range(world):
+        a = image_assignment(world, r)
+        for q in a.quadrants:
+            owners[q].append((r, a.side, a.peer))
+    for q, own in owners.items():
+        assert own, (world, q)
+        if len(own) == 1:
+            assert own[0][1] is None
+        else:
+            assert len(own) == 2
+            (r0, s0, p0), (r1, s1, p1) = own
+            assert {s0, s1} == {0, 1} and p0 == r1 and p1 == r0
+    busy = sum(1 for r in range(world) if image_assignment(world, r).quadrants)
+    assert busy == min(world, 2 * len(QUADRANTS))
+    if world == 8:
+        assert all(image_assignment(8, r).side == r % 2 for r in range(8))
 
 
 def _free_port():
