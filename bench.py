@@ -54,6 +54,7 @@ def parse():
                     help="replay one captured CUDA graph per step instead of launching through the API "
                          "(measured: no gain; programmatic dependent launch already hides the gaps)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-weak", action="store_true", help="skip the extra weak-scaling measurement at N > 1")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="batch configs on N GPUs: strong = BASELINE's one batch sharded 1/N per GPU "
                          "(images/s = batch / max t); weak = a whole batch per GPU")
@@ -311,10 +312,11 @@ def run_ours(args):
         scaling = "strong"
         sums_per_step = workloads.nominal_sums(args.config)
     else:
-        # a whole batch per rank, no collective on the data path (weak scaling)
+        # a whole batch per rank, no collective on the data path (weak scaling;
+        # at N = 1 both readings are the same workload: report the requested one)
         my_q = list(c.quadrants)
         imgs = workloads.make_images(args.config, c.batch, offset=rank * c.batch)
-        scaling = "weak"
+        scaling = "weak" if ws > 1 else (args.scaling if c.batch > 1 else "strong")
         sums_per_step = workloads.nominal_sums(args.config) * ws
     if not my_q:  # more ranks than work: this rank idles but joins the timing
         my_q = None
@@ -511,7 +513,7 @@ def run_ours(args):
         cpu["single_thread"] = cpu_single_thread(args.config, strategy, max(1.0, args.cpu_seconds / 2))
 
     weak = None
-    if ws > 1 and scaling == "strong" and c.batch > 1 and my_q is not None and not args.no_e2e:
+    if ws > 1 and scaling == "strong" and c.batch > 1 and my_q is not None and not args.no_weak:
         # extra key: the weak-scaling figure (a whole batch per GPU) beside the
         # strong-scaling headline
         wplan = fht.Plan(c.n, c.n, strategy, in_dtype=c.dtype, acc_dtype=c.acc, quadrants=my_q, batch=c.batch,
@@ -550,7 +552,9 @@ def run_ours(args):
                        "in_dtype": c.dtype, "acc_dtype": c.acc,
                        "parallelism": (f"batch-shard x{ws} ({c.batch}/{ws} images per GPU)" if c.batch > 1 and scaling == "strong"
                                        else f"batch per GPU x{ws}" if c.batch > 1
-                                       else "root-split x2 per quadrant" if ws > len(c.quadrants)
+                                       else "root-split x2 per quadrant" if ws >= 2 * len(c.quadrants)
+                                       else f"root-split x2 for {ws - len(c.quadrants)} of {len(c.quadrants)} quadrants"
+                                       if ws > len(c.quadrants)
                                        else f"quadrant-split x{ws}"),
                        "l2": "flushed between timed steps (512 MiB write, untimed)"},
             "images_per_s": round((c.batch * ws if scaling == "weak" else c.batch) / (ms_per_step * 1e-3), 1),

@@ -144,7 +144,9 @@ int fht_ipc_close(void* d_ptr);
  * root slopes [t_begin, t_end) of d_out (reference layout hough[s*W + t] or
  * native hough[t*H + s]):  OUT[t][s] = L[t0][s] + R[t1][(s + r) mod H]
  * (transform.cpp:46-57).  Used by the multi-GPU root split, where each GPU
- * owns one child and merges half the root.  Synchronises `stream`. */
+ * owns one child and merges half the root.  Stream ordered and asynchronous:
+ * the slope table is built once per (width, height, strategy, device) and
+ * cached on the device. */
 int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_dtype, int layout, const void* d_left,
                    int left_first, const void* d_right, int right_first, int t_begin, int t_end, void* d_out,
                    void* stream);

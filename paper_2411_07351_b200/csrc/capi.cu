@@ -192,6 +192,55 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+// One K2 window as copies for the TMA engine (k2_pair_pipe, FHT_K2_TMA):
+// rows (start + i) mod H, i < n, of a column (ld words allocated) into a
+// shared slot.  The window is placed at word `delta` of its slot so that the
+// long piece is a 16-byte aligned bulk copy (cp.async.bulk); the rest (the
+// part of a wrapping window whose alignment differs by H mod 4, and the <= 3
+// words before H rounded down) goes by 4-byte cp.async.  All word offsets.
+struct WinCopy {
+    int delta = 0, bulk_src = 0, bulk_dst = 0, bulk_words = 0, small_src = 0, small_dst = 0, small_n = 0;
+    bool ok = true;
+};
+WinCopy window_copy(int off, int n, int H, int ld) {
+    WinCopy c;
+    const int start = ((off % H) + H) % H;
+    if (n > H) {  // a window longer than the column (tiny H): all small copies
+        c.ok = false;
+        return c;
+    }
+    if (start + n <= H) {  // no wrap: one bulk copy (rounded up into the slot's slack)
+        c.delta = start & 3;
+        c.bulk_src = start - c.delta;
+        c.bulk_words = (n + c.delta + 3) & ~3;
+        c.ok = c.bulk_src + c.bulk_words <= ld;
+        return c;
+    }
+    const int a = H - start, b = n - a;  // [start, H) then [0, b)
+    const int h_al = H & ~3;
+    const int c1 = std::max(0, h_al - start);  // option 1: piece A in bulk up to H rounded down
+    if (n - c1 <= a) {
+        c.delta = start & 3;
+        if (c1 > 0) {
+            c.bulk_src = start - c.delta;
+            c.bulk_words = c1 + c.delta;
+        }
+        c.small_src = start + c1;  // wraps mod H in the kernel
+        c.small_dst = c.delta + c1;
+        c.small_n = n - c1;
+    } else {  // option 2: piece B in bulk (aligned at word 0), piece A small
+        c.delta = (4 - (a & 3)) & 3;
+        c.bulk_src = 0;
+        c.bulk_dst = c.delta + a;
+        c.bulk_words = (b + 3) & ~3;
+        c.small_src = start;
+        c.small_dst = c.delta;
+        c.small_n = a;
+        c.ok = c.bulk_words <= ld;
+    }
+    return c;
+}
+
 void upload(Group& g) {
     const SubPlan& sp = g.sp;
     // Width-32 non-root blocks go to the specialised K1P kernel (4-byte
@@ -269,6 +318,8 @@ void upload(Group& g) {
     struct PassOff {
         size_t tiles, loads, steps, ops, stores, bops, bops1 = 0, stores1 = 0;
         int pipe_delta = 0, pipe_loads = 0;
+        size_t twin = 0, tbops = 0, tbops1 = 0;  // TMA window records and their ops (0: none)
+        bool tma = false;
     };
     std::vector<PassOff> o_passes;
     for (const auto& ps : sp.passes) {
@@ -375,6 +426,46 @@ void upload(Group& g) {
                 o.stores1 = put(st1.data(), st1.size() * sizeof(int2));
                 o.pipe_delta = delta;
                 o.pipe_loads = maxl;
+                // TMA windows (one row tile of all D words, s0 = 0): every
+                // window's start is static, so the plan aligns it down to 16
+                // bytes and folds the residue into the ops' term offsets.
+                if (S >= g.pm_D && env_int("FHT_K2_TMA", 1, 0, 1) == 1) {
+                    std::vector<int4> twin, tb = bops, tb1 = b1;
+                    bool ok = true;
+                    for (const auto& t : ps.ptiles) {
+                        std::vector<int> delta_of(static_cast<size_t>(t.load_cnt), 0);
+                        for (int k = 0; k < t.load_cnt; ++k) {
+                            const auto& l = ps.loads[static_cast<size_t>(t.load_beg + k)];
+                            const WinCopy c = window_copy(l.off, static_cast<int>(S + l.ext), g.sp.H, g.ld);
+                            if (!c.ok) ok = false;
+                            delta_of[static_cast<size_t>(k)] = c.delta;
+                            const int dst = static_cast<int>(l.slot * L * 4);
+                            twin.push_back(make_int4(l.gcol, dst + 4 * c.bulk_dst, c.bulk_src, c.bulk_words));
+                            twin.push_back(make_int4(dst + 4 * c.small_dst, c.small_src, c.small_n, 0));
+                            if (l.slot != k) ok = false;  // window k lives in slot k (load-space slots)
+                        }
+                        const int ob = ps.pstep_offs[static_cast<size_t>(t.step_beg)];
+                        const int oe = ps.pstep_offs[static_cast<size_t>(t.step_beg + t.nsteps)];
+                        for (int oi = ob; oi < oe; ++oi) {
+                            const auto& op = ps.pops[static_cast<size_t>(oi)];
+                            int4* rec[2] = {&tb[2 * static_cast<size_t>(oi)], &tb1[2 * static_cast<size_t>(oi)]};
+                            for (int k = 0; k < op.nterms; ++k) {
+                                if (op.term[k].slot >= t.load_cnt) continue;  // an intermediate column
+                                const int add = 4 * delta_of[static_cast<size_t>(op.term[k].slot)];
+                                for (int4* r : rec) {
+                                    int& f = k == 0 ? r[0].w : k == 1 ? r[1].x : k == 2 ? r[1].y : r[1].z;
+                                    f += add;
+                                }
+                            }
+                        }
+                    }
+                    if (ok) {
+                        o.twin = put(twin.data(), twin.size() * sizeof(int4));
+                        o.tbops = put(tb.data(), tb.size() * sizeof(int4));
+                        o.tbops1 = put(tb1.data(), tb1.size() * sizeof(int4));
+                        o.tma = true;
+                    }
+                }
             }
         }
         o_passes.push_back(o);
@@ -402,6 +493,10 @@ void upload(Group& g) {
         d.stores1 = o.pipe_delta ? reinterpret_cast<const int2*>(base + o.stores1) : nullptr;
         d.pipe_delta = o.pipe_delta;
         d.pipe_loads = o.pipe_loads;
+        d.tma = o.tma ? 1 : 0;
+        d.twin = o.tma ? reinterpret_cast<const int4*>(base + o.twin) : nullptr;
+        d.tbops = o.tma ? reinterpret_cast<const int4*>(base + o.tbops) : nullptr;
+        d.tbops1 = o.tma ? reinterpret_cast<const int4*>(base + o.tbops1) : nullptr;
         d.tile_nc_max = 0;
         for (const auto& t : program(sp.passes[i], g.pairs).tiles) d.tile_nc_max = std::max(d.tile_nc_max, t.store_cnt);
         d.S = g.pass_S[i];
@@ -828,6 +923,33 @@ std::shared_ptr<fht_plan_s> cached_plan(int w, int h, int strategy, int acc, int
     return p;
 }
 
+// The root merge's slope table (t, t0, t1, r) per (W, H, strategy, device):
+// built and uploaded once, then shared (immutable) by every call, so the
+// multi-GPU root split's timed step neither allocates nor synchronises.  A
+// few bytes per slope; kept for the life of the process.
+const int4* merge_root_table(int width, int height, int strategy) {
+    static std::mutex mu;
+    static auto* tables = new std::map<std::tuple<int, int, int, int>, int4*>;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(width, height, strategy, dev);
+    auto it = tables->find(key);
+    if (it != tables->end()) return it->second;
+    const auto [w0, w1] = fhtb::split_width(width, strategy);
+    std::vector<int4> ops(static_cast<size_t>(width));
+    for (int t = 0; t < width; ++t) {  // transform.cpp:46-49
+        const int t0 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), width - 1));
+        const int t1 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), width - 1));
+        ops[static_cast<size_t>(t)] = make_int4(t, t0, t1, (t - t1) % height);
+    }
+    int4* d_ops = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&d_ops), ops.size() * sizeof(int4)), "cudaMalloc(merge table)");
+    cuda_check(cudaMemcpy(d_ops, ops.data(), ops.size() * sizeof(int4), cudaMemcpyHostToDevice), "H2D(merge table)");
+    tables->emplace(key, d_ops);
+    return d_ops;
+}
+
 size_t plan_cache_clear() {
     PlanCache& c = plan_cache();
     std::list<std::pair<CacheKey, std::shared_ptr<fht_plan_s>>> gone;
@@ -922,7 +1044,9 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
             for (int k = 0; k < g.qs.n; ++k) o << (k ? "," : "") << g.qs.code[k];
             o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"nbuf\":" << g.nbuf
               << ",\"level_pairs\":" << (g.pairs ? "true" : "false") << ",\"stage_pitch\":" << g.stage_pitch
-              << ",\"stage_bytes\":" << g.stage_img << ",\"u16_pair_D\":" << g.pm_D << ",\"pass_rows\":[";
+              << ",\"stage_bytes\":" << g.stage_img << ",\"u16_pair_D\":" << g.pm_D
+              << ",\"k2_tma_windows\":" << ((!g.dt.passes.empty() && g.dt.passes.back().tma) ? "true" : "false")
+              << ",\"pass_rows\":[";
             for (size_t k = 0; k < g.dt.passes.size(); ++k)
                 o << (k ? "," : "") << "[" << g.dt.passes[k].S << "," << g.dt.passes[k].L << "]";
             o << "],\"plan\":" << g.sp.describe() << "}";
@@ -1088,23 +1212,14 @@ int fht_merge_root(int width, int height, int strategy, int acc_dtype, int out_d
         if (!d_left || !d_right || !d_out) throw std::invalid_argument("merge_root: null pointer");
         if (t_begin < 0 || t_end > width || t_begin > t_end) throw std::invalid_argument("merge_root: bad slope range");
         if (layout != FHT_LAYOUT_REFERENCE && layout != FHT_LAYOUT_NATIVE) throw std::invalid_argument("unknown layout");
-        const auto [w0, w1] = fhtb::split_width(width, strategy);
-        std::vector<int4> ops(static_cast<size_t>(width));
-        for (int t = 0; t < width; ++t) {  // transform.cpp:46-49
-            const int t0 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w0 - 1), width - 1));
-            const int t1 = static_cast<int>(fhtb::round_half_up_ratio(static_cast<int64_t>(t) * (w1 - 1), width - 1));
-            ops[static_cast<size_t>(t)] = make_int4(t, t0, t1, (t - t1) % height);
-        }
+        if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED)
+            throw std::invalid_argument("unknown strategy (expected simple|tweaked)");
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        int4* d_ops = nullptr;
-        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_ops), ops.size() * sizeof(int4), st), "cudaMallocAsync");
-        cuda_check(cudaMemcpyAsync(d_ops, ops.data(), ops.size() * sizeof(int4), cudaMemcpyHostToDevice, st), "H2D");
+        const int4* d_ops = merge_root_table(width, height, strategy);
         const int rc = fhtb::launch_merge_root(d_ops, d_left, left_first, d_right, right_first, width, height, t_begin,
                                                t_end, d_out, acc_dtype, out_dtype, layout, st);
-        cudaFreeAsync(d_ops, st);
         if (rc < 0) throw std::invalid_argument("merge_root: unsupported (accumulator, output) dtype pair");
         cuda_check(cudaGetLastError(), "merge_root launch");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // the host op table goes out of scope
     });
 }
 

@@ -1791,6 +1791,27 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     }
 }
 
+// The TMA form of issue_windows for k2_pair_pipe (ps.tma): each window is one
+// 16-byte aligned bulk copy by the TMA engine (lane 0 of the warp that owns
+// it) plus at most one short run of 4-byte cp.async (the lanes) -- see
+// capi.cu window_copy.  Completion: the bulk bytes as mbarrier tx, the
+// 4-byte copies through every thread's cp.async.mbarrier.arrive.noinc (the
+// barrier counts all kThreads2 threads, so it cannot complete before every
+// expect_tx of the slot has been issued).
+__device__ __forceinline__ void issue_windows_tma(uint32_t srec, int nwin, const int* __restrict__ in, int ld,
+                                                  uint32_t stage, int H, int warp, int lane, uint32_t bar) {
+    constexpr int kW = kThreads2 / 32;
+    for (int w = warp; w < nwin; w += kW) {
+        const int4 r0 = lds4u(srec + 32u * w), r1 = lds4u(srec + 32u * w + 16u);
+        const int* __restrict__ col = in + (size_t)r0.x * ld;
+        if (lane == 0 && r0.w > 0) bulk_copy(stage + static_cast<uint32_t>(r0.y), col + r0.z, 4u * r0.w, bar);
+        uint32_t d = stage + static_cast<uint32_t>(r1.x) + 4u * lane;
+        int sw = r1.y + lane;
+        for (int i = lane; i < r1.z; i += 32, d += 128u, sw += 32) cp_async4(d, col + (sw >= H ? sw - H : sw));
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
 // ------------------------------------------------------- K2, pair mode
 // The u16 pair mode root band with double-buffered windows: each CTA keeps
 // its tile and walks slots (grid.z strided).  While slot i computes, the
@@ -1798,7 +1819,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
 // moved by ps.pipe_delta; the op and store tables carry both variants), so
 // the copies' latency hides behind the merges.  Tiles of <= 16 slopes,
 // reference layout only (the launcher falls back to k2_pass MODE 6).
-template <class Out>
+template <class Out, bool TMA>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const int* __restrict__ src,
                                                           long long slot_elems, int W, int H, int ld, OutDesc out,
                                                           QuadSet qs, int img0, int pmD, int nslots) {
@@ -1819,9 +1840,13 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
     int* ssteps = reinterpret_cast<int*>(sbops + 4 * ps.max_tile_ops);
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid] - op0;
-    for (int k = tid; k < 2 * nops; k += kThreads2) {
-        sbops[k] = ps.bops[2 * op0 + k];
-        sbops[2 * nops + k] = ps.bops1[2 * op0 + k];
+    {
+        const int4* __restrict__ b0 = TMA ? ps.tbops : ps.bops;
+        const int4* __restrict__ b1 = TMA ? ps.tbops1 : ps.bops1;
+        for (int k = tid; k < 2 * nops; k += kThreads2) {
+            sbops[k] = b0[2 * op0 + k];
+            sbops[2 * nops + k] = b1[2 * op0 + k];
+        }
     }
     const int nc = tile.store_cnt;
     const int t0 = ps.stores[tile.store_beg].y;
@@ -1831,21 +1856,49 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
     // the window records, after the step offsets: each warp copies the
     // entries it will issue (so a __syncwarp orders them)
     const uint32_t srec = smem_u32(ssteps + 64);
-    for (int mine = warp + kWarps * lane; mine < tile.load_cnt; mine += 32 * kWarps)
-        sts4u(srec + 16u * mine, ps.loads[tile.load_beg + mine]);
-    __syncwarp();
+    // TMA: two window records per load, then the two buffers' mbarriers
+    const uint32_t bars = srec + (TMA ? 32u : 16u) * static_cast<uint32_t>(ps.pipe_loads);
+    if constexpr (TMA) {
+        for (int k = warp; k < tile.load_cnt; k += kWarps)  // each warp stages the records it will issue
+            if (lane < 2) sts4u(srec + 32u * k + 16u * lane, ps.twin[2 * tile.load_beg + 2 * k + lane]);
+        if (tid == 0) {
+            mbar_init(bars, kThreads2);
+            mbar_init(bars + 8u, kThreads2);
+        }
+        __syncthreads();
+    } else {
+        for (int mine = warp + kWarps * lane; mine < tile.load_cnt; mine += 32 * kWarps)
+            sts4u(srec + 16u * mine, ps.loads[tile.load_beg + mine]);
+        __syncwarp();
+    }
     grid_dep_wait();
-    issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
-    cp_async_commit();
+    if constexpr (TMA) {
+        issue_windows_tma(srec, tile.load_cnt, src + (size_t)slot * slot_elems, ld, sbase, H, warp, lane, bars);
+    } else {
+        issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
+        cp_async_commit();
+    }
     for (int it = 0;; ++it) {
         const int p = it & 1;
-        cp_async_wait0();  // this slot's windows
+        if constexpr (TMA) {
+            mbar_wait(bars + 8u * p, (it >> 1) & 1);  // this slot's windows (bulk bytes + 4-byte copies)
+        } else {
+            cp_async_wait0();  // this slot's windows
+        }
         __syncthreads();   // ... visible to all; the last slot's store is done with the other buffer
         const int next = slot + static_cast<int>(gridDim.z);
         if (next < nslots) {
-            issue_windows<Acc>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H, ld,
-                               warp, lane, 0u, srec);
-            cp_async_commit();
+            if constexpr (TMA) {
+                // the other buffer was last read (and some of its slots
+                // written) through the generic proxy before the barrier above
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_windows_tma(srec, tile.load_cnt, src + (size_t)next * slot_elems, ld, sbase + (p ? 0u : alt), H,
+                                  warp, lane, bars + 8u * (1 - p));
+            } else {
+                issue_windows<Acc>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H, ld,
+                                   warp, lane, 0u, srec);
+                cp_async_commit();
+            }
         }
         const int4* ops = sbops + (p ? 2 * nops : 0);
         for (int k = 0; k < tile.nsteps; ++k) {
@@ -2055,9 +2108,11 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             (void)max_nc;
             if (g.pm_D && final_pass && ps.pairs && ps.pipe_delta > 0 && !g.k2_bulk && g.out.layout == 0 &&
                 ps.tile_nc_max <= 16) {
+                const bool tma = ps.tma && ps.twin != nullptr;
                 const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops) +
-                                   static_cast<size_t>(ps.pipe_loads) * sizeof(int4);  // + the window records
-                auto kp = k2_pair_pipe<Out>;
+                                   static_cast<size_t>(ps.pipe_loads) * sizeof(int4) * (tma ? 2 : 1) +  // window records
+                                   (tma ? 16 : 0);                                                       // mbarriers
+                auto kp = tma ? k2_pair_pipe<Out, true> : k2_pair_pipe<Out, false>;
                 allow_smem(reinterpret_cast<const void*>(kp));
                 const int rt = (g.pm_D + ps.S - 1) / ps.S;
                 const int spc = slots_per_cta(rt * ps.ntiles * nslots, nslots);

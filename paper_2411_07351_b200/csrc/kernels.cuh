@@ -68,6 +68,15 @@ struct PassDev {
     const int2* stores1;
     int pipe_delta, pipe_loads;  // slot offset of the second buffer, its size (max load_cnt)
     int tile_nc_max;             // most stored slopes of one tile
+    // TMA windows for k2_pair_pipe (tma = 1; one row tile, s0 = 0): per load,
+    // {gcol, bulk dst byte, bulk src word, bulk words}, {small dst byte, small
+    // src word (wraps mod H), small count, 0}; dst bytes are relative to the
+    // window buffer; tbops / tbops1 = bops / bops1 with every window term
+    // moved by its window's alignment residue
+    int tma;
+    const int4* twin;
+    const int4* tbops;
+    const int4* tbops1;
 };
 
 struct GroupLaunch {

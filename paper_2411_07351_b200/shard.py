@@ -193,7 +193,13 @@ class GpuRootBackend:
         if not hasattr(self, "_peers"):
             self._peers = {}
         if key not in self._peers:
-            self._peers[key] = PeerExchange(nbytes, device, peer, group)
+            import torch.distributed as dist
+
+            # the store tag both ranks of the pair derive alike: the pair and
+            # the quadrant / shape (not the side, which differs between them)
+            quadrant, _side, W, H = key
+            pair = "-".join(str(r) for r in sorted((dist.get_rank(), peer)))
+            self._peers[key] = PeerExchange(nbytes, device, peer, group, key=f"{pair}/{quadrant}/{W}x{H}")
         return self._peers[key]
 
     def merge(self, split: RootSplit, left, left_first, right, right_first, t_beg, t_end, out):
@@ -212,12 +218,21 @@ class GpuRootBackend:
                                    ctypes.c_void_p(lp), left_first, ctypes.c_void_p(rp), right_first, t_beg, t_end,
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
 
-    def empty_out(self, split: RootSplit, like):
+    def empty_out(self, split: RootSplit, like, key=None):
+        """The root output buffer: full size, each side writes only its own
+        slopes.  With a `key` it is allocated once and reused every step (the
+        other side's slopes are left as they are -- uninitialised)."""
         import torch
 
         dt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[self.out_dtype]
         shape = (split.H, split.W) if self.layout == "reference" else (split.W, split.H)
-        return torch.zeros(shape, dtype=dt, device=like.device)
+        if key is None:
+            return torch.zeros(shape, dtype=dt, device=like.device)
+        if not hasattr(self, "_outs"):
+            self._outs = {}
+        if key not in self._outs:
+            self._outs[key] = torch.empty(shape, dtype=dt, device=like.device)
+        return self._outs[key]
 
 
 class PeerExchange:
@@ -225,24 +240,106 @@ class PeerExchange:
     buffer the peer writes its child slopes into (exported as a CUDA IPC
     handle), and the peer's buffer opened here.  Handles travel once over the
     process group (any backend); the data never does -- the child transform's
-    last pass stores it straight into peer memory over NVLink."""
+    last pass stores it straight into peer memory over NVLink.
 
-    def __init__(self, nbytes: int, device: int, peer: int, group=None):
+    Per step the two sides are ordered on the device, with no stream
+    synchronisation and no collective: two interprocess CUDA events per side
+    ("my peer stores have landed", "I am done reading my receive buffer"),
+    waited with cudaStreamWaitEvent on the other side.  cudaStreamWaitEvent
+    binds to an event's most recent record, so a side must not wait before
+    the peer has *issued* this step's record: two host counters in a shared
+    memory segment (the ranks of a pair share a node) carry "record k issued"
+    -- a host flag, not a device sync; the GPU queue keeps running ahead."""
+
+    TIMEOUT_S = 120.0
+
+    def __init__(self, nbytes: int, device: int, peer: int, group=None, key: str = "0"):
         import ctypes
 
+        import torch
         import torch.distributed as dist
 
         from ._lib import check, lib
 
+        self.key = key
         self.local = ctypes.c_void_p()
         check(lib().fht_device_alloc(max(1, nbytes), device, ctypes.byref(self.local)))
         handle = ctypes.create_string_buffer(64)
         check(lib().fht_ipc_get_handle(self.local, handle, 64))
-        got = [None] * dist.get_world_size(group)
-        dist.all_gather_object(got, (dist.get_rank(), handle.raw), group=group)
-        peer_handle = dict(got)[peer]
+        self.rank, self.peer = dist.get_rank(), peer
+        self.side = 0 if self.rank < peer else 1
+        self.dev = torch.device("cuda", device)
+        # my events: 0 = peer stores issued by me have landed, 1 = my receive buffer is free
+        self.ev = [torch.cuda.Event(enable_timing=False, blocking=False, interprocess=True) for _ in range(2)]
+        for e in self.ev:
+            e.record(torch.cuda.current_stream(self.dev))  # an IPC handle needs a recorded event
+        torch.cuda.current_stream(self.dev).synchronize()
+        shm_name = None
+        if self.side == 0:
+            from multiprocessing import shared_memory
+
+            self._shm = shared_memory.SharedMemory(create=True, size=64)
+            shm_name = self._shm.name
+        # the handles travel through the process group's key-value store: only
+        # the two ranks of the pair take part (other ranks may be doing other
+        # work, e.g. a quadrant of their own)
+        import pickle
+
+        from torch.distributed import distributed_c10d as c10d
+
+        store = c10d._get_default_store()  # noqa: SLF001
+        tag = f"fht_root_split/{self.key}"
+        store.set(f"{tag}/{self.rank}", pickle.dumps((handle.raw, [e.ipc_handle() for e in self.ev], shm_name)))
+        peer_handle, peer_ev, peer_shm = pickle.loads(store.get(f"{tag}/{peer}"))
         self.remote = ctypes.c_void_p()
         check(lib().fht_ipc_open_handle(peer_handle, 64, device, ctypes.byref(self.remote)))
+        self.peer_ev = [torch.cuda.Event.from_ipc_handle(self.dev, h) for h in peer_ev]
+        if self.side == 1:
+            from multiprocessing import resource_tracker, shared_memory
+
+            self._shm = shared_memory.SharedMemory(name=peer_shm)
+            # the creator (side 0) owns the segment's lifetime
+            resource_tracker.unregister(self._shm._name, "shared_memory")  # noqa: SLF001
+        import numpy as np
+
+        # counters[side * 2 + e]: the step whose record of event e that side has issued
+        self.counters = np.ndarray((4,), dtype=np.int64, buffer=self._shm.buf)
+        if self.side == 0:
+            self.counters[:] = 0
+        self.step = 0
+
+    def _await(self, who: int, e: int, k: int):
+        import time
+
+        t0 = time.monotonic()
+        spins = 0
+        while self.counters[who * 2 + e] < k:
+            spins += 1
+            if spins > 1000:
+                time.sleep(0)
+                if time.monotonic() - t0 > self.TIMEOUT_S:
+                    raise RuntimeError("root split: the peer stopped responding")
+
+    def begin(self, stream):
+        """Before this step's child transform writes into the peer's buffer:
+        wait (on the device) until the peer has finished reading it."""
+        self.step += 1
+        if self.step > 1:
+            self._await(1 - self.side, 1, self.step - 1)
+            stream.wait_event(self.peer_ev[1])
+
+    def stored(self, stream):
+        """After the child transform: publish "my stores into the peer landed"
+        and wait (on the device) for the peer's stores into my buffer."""
+        self.ev[0].record(stream)
+        self.counters[self.side * 2] = self.step
+        self._await(1 - self.side, 0, self.step)
+        stream.wait_event(self.peer_ev[0])
+
+    def consumed(self, stream):
+        """After the merge: my receive buffer may be overwritten again."""
+        self.ev[1].record(stream)
+        self.counters[self.side * 2 + 1] = self.step
 
     def close(self):
         from ._lib import lib
@@ -253,6 +350,13 @@ class PeerExchange:
         if self.local:
             lib().fht_device_free(self.local)
             self.local = None
+        shm = getattr(self, "_shm", None)
+        if shm is not None:
+            self.counters = None
+            shm.close()
+            if self.side == 0:
+                shm.unlink()
+            self._shm = None
 
 
 def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: int | None = None, group=None,
@@ -286,17 +390,17 @@ def root_split_quadrant(img, quadrant: str, strategy, side: int, backend, peer: 
         esz = torch.empty((), dtype={"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[backend.acc_dtype]
                           ).element_size()
         ex = backend.peer_exchange((quadrant, side, W, H), max(rhi - rlo, hi - lo) * H * esz, dev, peer, group)
-        torch.cuda.current_stream(img.device).synchronize()
-        dist.barrier(group)  # the peer is done reading its buffer from the previous step
+        st = torch.cuda.current_stream(img.device)
+        ex.begin(st)  # device wait: the peer is done reading its buffer from the previous step
         mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side, peer_ptr=ex.remote.value,
                              peer_cols=(lo, hi))
-        torch.cuda.current_stream(img.device).synchronize()
-        dist.barrier(group)  # both sides' peer stores have landed
-        out = backend.empty_out(sp, mine)
+        ex.stored(st)  # device wait: the peer's stores into my buffer have landed
+        out = backend.empty_out(sp, mine, key=(quadrant, side, W, H))
         if side == 0:
             backend.merge(sp, mine, 0, ex.local.value, rlo, 0, sp.t_mid, out)
         else:
             backend.merge(sp, ex.local.value, rlo, mine, 0, sp.t_mid, W, out)
+        ex.consumed(st)
         return out, sp
     mine = backend.child(child_view(img, quadrant, side, sp), quadrant, side)
     # gloo moves host tensors only: stage the exchange through host memory

@@ -38,10 +38,10 @@ def _root_worker(rank, port, out, exchange):
     sys.path.insert(0, str(ROOT))
     from paper_2411_07351_b200 import shard
 
-    rng = np.random.default_rng(9)
-    img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
     be = shard.GpuRootBackend("tweaked", "f32", "f32")
-    for _ in range(2):  # twice: the receive buffers are reused across steps
+    for k in range(3):  # three steps, a new image each: buffers, events and counters are reused across steps
+        rng = np.random.default_rng(9 + k)
+        img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
         res, sp = shard.root_split_quadrant(img, "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
     torch.cuda.synchronize()
     np.save(f"{out}.{rank}.npy", res.cpu().numpy())
@@ -59,7 +59,7 @@ def test_root_split_two_processes_one_gpu(tmp_path, exchange):
 
     out = tmp_path / "rs"
     mp.spawn(_root_worker, args=(_port(), str(out), exchange), nprocs=2, join=True)
-    rng = np.random.default_rng(9)
+    rng = np.random.default_rng(11)  # the last step's image
     img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
     full = fht.Plan(2049, 1500, "tweaked", in_dtype="f32", acc_dtype="f32", quadrants=["vert_pos"])(img[None])
     ref = full["vert_pos"][0].cpu().numpy()
@@ -82,9 +82,24 @@ def _torchrun(n, *args):
 
 
 def test_bench_two_ranks_batch_shards():
+    """BASELINE c4 on N GPUs: the one 256-image batch sharded 128 + 128."""
     d = _torchrun(2)
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
-    assert d["config"]["parallelism"] == "batch-shard x2"
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("batch-shard x2") and d["config"]["images_per_gpu"] == 128
+    assert d["images_per_s"] == pytest.approx(256 / (d["ms_per_step"] * 1e-3), rel=1e-2)
+    w = d["weak_scaling"]
+    assert w["images_per_gpu"] == 256 and w["value"] > 0
+
+
+def test_bench_two_ranks_weak():
+    d = _torchrun(2, "--scaling", "weak", "--no-weak")
+    assert d["scaling"] == "weak" and d["config"]["images_per_gpu"] == 256 and d["weak_scaling"] is None
+
+
+def test_bench_six_ranks_every_quadrant_owned():
+    """6 ranks on one image: two quadrants root-split, two whole (image_assignment)."""
+    d = _torchrun(6, "--config", "c3", "--no-weak")
+    assert d["n_gpus"] == 6 and d["scaling"] == "strong" and d["value"] > 0
 
 
 def test_bench_eight_ranks_root_split_c5():

@@ -168,3 +168,25 @@ def test_pair_mode_chunks_and_graph_replay(monkeypatch):
     for i, ref in refs.items():
         for k in Q:
             np.testing.assert_array_equal(out[k][i].cpu().numpy(), ref[k], err_msg=f"graph img{i} {k}")
+
+
+@pytest.mark.parametrize("h,w,strategy", [(509, 509, 1), (512, 512, 1), (64, 65, 1), (65, 300, 0), (130, 257, 1),
+                                          (333, 77, 0), (257, 511, 1)])
+def test_tma_windows_match_cp_async_windows(monkeypatch, h, w, strategy):
+    """The pair-mode root band's windows by the TMA engine (bulk copies, the
+    window starts aligned down and the residue folded into the ops) against
+    the same band with 4/16-byte cp.async windows, and both against the oracle."""
+    rng = np.random.default_rng(h + 7 * w)
+    imgs = rng.integers(0, 256, (9, h, w), dtype=np.uint8)
+    imgs[3] = 255
+    out, desc = _run(imgs, strategy)
+    assert any(g["k2_tma_windows"] for g in desc["groups"]), desc
+    monkeypatch.setenv("FHT_K2_TMA", "0")
+    out0, desc0 = _run(imgs, strategy)
+    assert not any(g["k2_tma_windows"] for g in desc0["groups"])
+    for k in Q:
+        np.testing.assert_array_equal(out[k], out0[k])
+    for bi in (0, 3, 8):
+        ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+        for k in Q:
+            np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} {k} img{bi}")
