@@ -652,7 +652,11 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             for (int k = 0; k < g->qs.n; ++k) (codes[static_cast<size_t>(k)] < 2 ? need_t : need_p) = true;
             const long long ntile = (H + S - 1) / S;
             // pair mode: rows [0, 2D + 31) (the upper half of every word is D rows on)
-            g->stage_pitch = ((pm ? 2LL * pmD : ntile * S) + 36 + 15) / 16 * 16;
+            // FHT_STAGE_ALIGN=128 starts every column on a 128-byte line (a warp's
+            // 4-byte loads of 32 row chunks then touch one line, not two):
+            // measured slower (the staging writes grow 14 %, K1P unchanged)
+            const long long al = env_int("FHT_STAGE_ALIGN", 16, 16, 128);
+            g->stage_pitch = ((pm ? 2LL * pmD : ntile * S) + 36 + al - 1) / al * al;
             const long long set = static_cast<long long>(W) * g->stage_pitch;
             g->stage_t = need_t ? 0 : -1;
             g->stage_p = need_p ? (need_t ? set : 0) : -1;

@@ -1469,11 +1469,11 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
 // srec != 0: the tile's records were copied to shared memory (k2_pair_pipe,
 // which issues the same tile's windows once per slot), each warp's own
 // entries only -- a shared load instead of a global one per slot.
-template <class Acc>
+template <class Acc, int NT = kThreads2>
 __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileDev& tile, const Acc* __restrict__ in,
                                               uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
                                               int lane, uint32_t bar, uint32_t srec = 0u) {
-    constexpr int kW = kThreads2 / 32;
+    constexpr int kW = NT / 32;
     for (int base = 0; base < tile.load_cnt; base += 32 * kW) {
         const int mine = base + warp + kW * lane;
         const int4 rec = mine < tile.load_cnt ? (srec ? lds4u(srec + 16u * mine) : ps.loads[tile.load_beg + mine])
@@ -1798,9 +1798,10 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
 // 4-byte copies through every thread's cp.async.mbarrier.arrive.noinc (the
 // barrier counts all kThreads2 threads, so it cannot complete before every
 // expect_tx of the slot has been issued).
+template <int NT = kThreads2>
 __device__ __forceinline__ void issue_windows_tma(uint32_t srec, int nwin, const int* __restrict__ in, int ld,
                                                   uint32_t stage, int H, int warp, int lane, uint32_t bar) {
-    constexpr int kW = kThreads2 / 32;
+    constexpr int kW = NT / 32;
     for (int w = warp; w < nwin; w += kW) {
         const int4 r0 = lds4u(srec + 32u * w), r1 = lds4u(srec + 32u * w + 16u);
         const int* __restrict__ col = in + (size_t)r0.x * ld;
@@ -1819,12 +1820,16 @@ __device__ __forceinline__ void issue_windows_tma(uint32_t srec, int nwin, const
 // moved by ps.pipe_delta; the op and store tables carry both variants), so
 // the copies' latency hides behind the merges.  Tiles of <= 16 slopes,
 // reference layout only (the launcher falls back to k2_pass MODE 6).
-template <class Out, bool TMA>
-__global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const int* __restrict__ src,
-                                                          long long slot_elems, int W, int H, int ld, OutDesc out,
-                                                          QuadSet qs, int img0, int pmD, int nslots) {
+// WIDE: tiles of 17..32 slopes on 1024 threads, one CTA per SM (the two
+// window buffers of a 32-slope tile take ~175 KB): half the root store's
+// partial-line writes and fewer windows per slope than 16-slope tiles.
+template <class Out, bool TMA, bool WIDE = false>
+__global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
+    k2_pair_pipe(PassDev ps, const int* __restrict__ src, long long slot_elems, int W, int H, int ld, OutDesc out,
+                 QuadSet qs, int img0, int pmD, int nslots) {
     using Acc = int;
-    constexpr int kWarps = kThreads2 / 32;
+    constexpr int kNT = WIDE ? 1024 : kThreads2;
+    constexpr int kWarps = kNT / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1843,15 +1848,16 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
     {
         const int4* __restrict__ b0 = TMA ? ps.tbops : ps.bops;
         const int4* __restrict__ b1 = TMA ? ps.tbops1 : ps.bops1;
-        for (int k = tid; k < 2 * nops; k += kThreads2) {
+        for (int k = tid; k < 2 * nops; k += kNT) {
             sbops[k] = b0[2 * op0 + k];
             sbops[2 * nops + k] = b1[2 * op0 + k];
         }
     }
     const int nc = tile.store_cnt;
     const int t0 = ps.stores[tile.store_beg].y;
-    const int xs0 = (lane & 15) < nc ? ps.stores[tile.store_beg + (lane & 15)].x : 0;
-    const int xs1 = (lane & 15) < nc ? ps.stores1[tile.store_beg + (lane & 15)].x : 0;
+    const int sl = WIDE ? lane : (lane & 15);  // the slope whose root slots this lane stores
+    const int xs0 = sl < nc ? ps.stores[tile.store_beg + sl].x : 0;
+    const int xs1 = sl < nc ? ps.stores1[tile.store_beg + sl].x : 0;
     const int rows = min(S, pmD - s0), rows_hi = max(0, min(rows, H - pmD - s0));
     // the window records, after the step offsets: each warp copies the
     // entries it will issue (so a __syncwarp orders them)
@@ -1862,8 +1868,8 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
         for (int k = warp; k < tile.load_cnt; k += kWarps)  // each warp stages the records it will issue
             if (lane < 2) sts4u(srec + 32u * k + 16u * lane, ps.twin[2 * tile.load_beg + 2 * k + lane]);
         if (tid == 0) {
-            mbar_init(bars, kThreads2);
-            mbar_init(bars + 8u, kThreads2);
+            mbar_init(bars, kNT);
+            mbar_init(bars + 8u, kNT);
         }
         __syncthreads();
     } else {
@@ -1873,9 +1879,9 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
     }
     grid_dep_wait();
     if constexpr (TMA) {
-        issue_windows_tma(srec, tile.load_cnt, src + (size_t)slot * slot_elems, ld, sbase, H, warp, lane, bars);
+        issue_windows_tma<kNT>(srec, tile.load_cnt, src + (size_t)slot * slot_elems, ld, sbase, H, warp, lane, bars);
     } else {
-        issue_windows<Acc>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
+        issue_windows<Acc, kNT>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
         cp_async_commit();
     }
     for (int it = 0;; ++it) {
@@ -1892,19 +1898,22 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
                 // the other buffer was last read (and some of its slots
                 // written) through the generic proxy before the barrier above
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_windows_tma(srec, tile.load_cnt, src + (size_t)next * slot_elems, ld, sbase + (p ? 0u : alt), H,
+                issue_windows_tma<kNT>(srec, tile.load_cnt, src + (size_t)next * slot_elems, ld, sbase + (p ? 0u : alt), H,
                                   warp, lane, bars + 8u * (1 - p));
             } else {
-                issue_windows<Acc>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H, ld,
-                                   warp, lane, 0u, srec);
+                issue_windows<Acc, kNT>(ps, tile, src + (size_t)next * slot_elems, sbase + (p ? 0u : alt), L, S, s0, H,
+                                        ld, warp, lane, 0u, srec);
                 cp_async_commit();
             }
         }
         const int4* ops = sbops + (p ? 2 * nops : 0);
         for (int k = 0; k < tile.nsteps; ++k) {
             if (k) __syncthreads();
-            if (k + 1 < tile.nsteps) run_step_terms<Acc, kWarps, false>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
-            else run_step_widen<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+            if (k + 1 < tile.nsteps) {
+                run_step_terms<Acc, kWarps, false>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+            } else {
+                run_step_widen<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+            }
         }
         __syncthreads();
         int img_l, qi;
@@ -1912,11 +1921,19 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pair_pipe(PassDev ps, const i
         Out* __restrict__ o =
             reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
         const int xs = p ? xs1 : xs0;
-        store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs & 0xffff) * L * 4u, s0,
-                                            rows, warp, lane);
-        if (rows_hi > 0)
-            store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs >> 16) * L * 4u,
-                                                s0 + pmD, rows_hi, warp, lane);
+        if constexpr (WIDE) {
+            store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs & 0xffff) * L * 4u, 0u, s0,
+                                              rows, warp, lane);
+            if (rows_hi > 0)
+                store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs >> 16) * L * 4u, 0u,
+                                                  s0 + pmD, rows_hi, warp, lane);
+        } else {
+            store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs & 0xffff) * L * 4u, s0,
+                                                rows, warp, lane);
+            if (rows_hi > 0)
+                store_root_rows16<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs >> 16) * L * 4u,
+                                                    s0 + pmD, rows_hi, warp, lane);
+        }
         slot = next;
         if (slot >= nslots) break;
     }
@@ -2107,17 +2124,19 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             int max_nc = 0;
             (void)max_nc;
             if (g.pm_D && final_pass && ps.pairs && ps.pipe_delta > 0 && !g.k2_bulk && g.out.layout == 0 &&
-                ps.tile_nc_max <= 16) {
+                ps.tile_nc_max <= 32) {
+                const bool wide = ps.tile_nc_max > 16;
                 const bool tma = ps.tma && ps.twin != nullptr;
                 const size_t smp = k2_smem_bytes(g.acc_dtype, ps.pipe_delta + ps.pipe_loads, ps.L, 2 * ps.max_tile_ops) +
                                    static_cast<size_t>(ps.pipe_loads) * sizeof(int4) * (tma ? 2 : 1) +  // window records
-                                   (tma ? 16 : 0);                                                       // mbarriers
-                auto kp = tma ? k2_pair_pipe<Out, true> : k2_pair_pipe<Out, false>;
+                                   16;                                                                   // mbarriers
+                auto kp = wide ? (tma ? k2_pair_pipe<Out, true, true> : k2_pair_pipe<Out, false, true>)
+                               : (tma ? k2_pair_pipe<Out, true> : k2_pair_pipe<Out, false>);
                 allow_smem(reinterpret_cast<const void*>(kp));
                 const int rt = (g.pm_D + ps.S - 1) / ps.S;
                 const int spc = slots_per_cta(rt * ps.ntiles * nslots, nslots);
                 dim3 gp(rt, ps.ntiles, (nslots + spc - 1) / spc);
-                launch_k(g.pdl, kp, gp, dim3(kThreads2), smp, st, pd, SRC, slot_elems, g.W, g.H, g.ld, g.out, g.qs,
+                launch_k(g.pdl, kp, gp, dim3(wide ? 1024 : kThreads2), smp, st, pd, SRC, slot_elems, g.W, g.H, g.ld, g.out, g.qs,
                          g.img0, g.pm_D, nslots);
                 ++launches;
                 if (hook) hook(ctx, 3);

@@ -190,3 +190,22 @@ def test_tma_windows_match_cp_async_windows(monkeypatch, h, w, strategy):
         ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
         for k in Q:
             np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} {k} img{bi}")
+
+
+@pytest.mark.parametrize("h,w,strategy", [(509, 509, 1), (65, 300, 0), (257, 511, 1), (100, 300, 1)])
+def test_wide_root_band_tiles(monkeypatch, h, w, strategy):
+    """32-slope root-band tiles on the 1024-thread pair kernel (an option:
+    FHT_TILE_WIDTH=32 with the shared-memory budget raised), TMA windows on
+    and off, against the oracle."""
+    rng = np.random.default_rng(h * 3 + w)
+    imgs = rng.integers(0, 256, (3, h, w), dtype=np.uint8)
+    imgs[1] = 255
+    monkeypatch.setenv("FHT_TILE_WIDTH", "32")
+    monkeypatch.setenv("FHT_K2_SMEM_KB", "125")
+    for tma in ("1", "0"):
+        monkeypatch.setenv("FHT_K2_TMA", tma)
+        out, desc = _run(imgs, strategy)
+        for bi in range(3):
+            ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+            for k in Q:
+                np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} tma{tma} {k} img{bi}")
