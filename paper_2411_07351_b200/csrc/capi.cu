@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <list>
@@ -106,9 +107,12 @@ struct Group {
     std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
     int pm_D = 0;  // u16 pair mode (0: off): workspace words pair rows j and j + pm_D
     size_t slot_bytes = 0;
+    size_t acc_sz = 4;  // accumulator bytes
 };
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+bool esize_acc4(const Group& g) { return g.acc_sz == 4; }
 
 constexpr int kHostStreams = 3;
 
@@ -241,6 +245,49 @@ WinCopy window_copy(int off, int n, int H, int ld) {
     return c;
 }
 
+// For a tile of a level-pair program: for every op term, whether it reads a
+// window as loaded (its slot < load_cnt and not yet overwritten by an op of
+// an earlier step; slots written in a step are read no earlier than the next
+// step), and for every store whether its slot still holds a window (a copy
+// tile).  TMA windows sit at a per-window word offset (alignment residue):
+// exactly these reads must add it.
+struct WindowReads {
+    std::vector<std::array<int, 4>> term_window;  // per op of the tile: window index or -1
+    std::vector<int> store_window;                // per store of the tile: window index or -1
+};
+WindowReads window_reads(const fhtb::FusedPass& ps, const fhtb::PassTile& t) {
+    WindowReads w;
+    std::vector<int> holds(static_cast<size_t>(std::max(ps.pmax_slots, t.load_cnt) + 1), -1);
+    for (int k = 0; k < t.load_cnt; ++k) holds[static_cast<size_t>(k)] = k;
+    for (int st = 0; st < t.nsteps; ++st) {
+        const int ob = ps.pstep_offs[static_cast<size_t>(t.step_beg + st)];
+        const int oe = ps.pstep_offs[static_cast<size_t>(t.step_beg + st + 1)];
+        for (int oi = ob; oi < oe; ++oi) {
+            const auto& op = ps.pops[static_cast<size_t>(oi)];
+            std::array<int, 4> tw = {-1, -1, -1, -1};
+            for (int k = 0; k < op.nterms; ++k) {
+                const size_t sl = static_cast<size_t>(op.term[k].slot);
+                tw[static_cast<size_t>(k)] = sl < holds.size() ? holds[sl] : -1;
+            }
+            w.term_window.push_back(tw);
+        }
+        for (int oi = ob; oi < oe; ++oi) {  // this step's outputs replace what their slots held
+            const auto& op = ps.pops[static_cast<size_t>(oi)];
+            for (int d : {op.dst, op.dst_hi})
+                if (d >= 0) {
+                    if (static_cast<size_t>(d) >= holds.size()) holds.resize(static_cast<size_t>(d) + 1, -1);
+                    holds[static_cast<size_t>(d)] = -1;
+                }
+        }
+    }
+    for (int k = 0; k < t.store_cnt; ++k) {
+        const auto& st = ps.pstores[static_cast<size_t>(t.store_beg + k)];
+        const size_t sl = static_cast<size_t>(st.slot);
+        w.store_window.push_back(sl < holds.size() ? holds[sl] : -1);
+    }
+    return w;
+}
+
 void upload(Group& g) {
     const SubPlan& sp = g.sp;
     // Width-32 non-root blocks go to the specialised K1P kernel (4-byte
@@ -320,6 +367,8 @@ void upload(Group& g) {
         int pipe_delta = 0, pipe_loads = 0;
         size_t twin = 0, tbops = 0, tbops1 = 0;  // TMA window records and their ops (0: none)
         bool tma = false;
+        size_t kwslots = 0, kwstores = 0;  // TMA windows in k2_pass (level pairs)
+        bool ktma = false;
     };
     std::vector<PassOff> o_passes;
     for (const auto& ps : sp.passes) {
@@ -383,6 +432,45 @@ void upload(Group& g) {
                                          static_cast<int>(S + op.ext)));
             }
             o.bops = put(bops.data(), bops.size() * sizeof(int4));
+            // TMA windows for the level-pair k2_pass (row tiles: the windows'
+            // starts, so their alignment residues, depend on the row tile and
+            // are applied at run time): per op, the window index each term
+            // reads (4 x u8, 0xff: an intermediate column); per store, bit 30
+            // of the column marks a stored window (a copy tile)
+            // (opt-in, FHT_K2_TMA_BANDS=1: measured slower -- these CTAs load one
+            // row tile and then compute, so the bulk copies' latency is exposed;
+            // c5 bands 0.684 / 0.900 -> 0.712 / 0.967 ms)
+            if (g.pairs && esize_acc4(g) && env_int("FHT_K2_TMA_BANDS", 0, 0, 1) == 1) {
+                bool ok = true;
+                std::vector<int> wslots(ps.pops.size(), -1);
+                std::vector<int2> wstores;
+                for (const auto& st : pr.stores) wstores.push_back(make_int2(st.slot, st.gcol));
+                for (const auto& t : ps.ptiles) {
+                    if (t.load_cnt > 64) ok = false;  // residues of <= 64 windows live in two 64-bit masks
+                    for (int k = 0; k < t.load_cnt; ++k) {
+                        const auto& l = ps.loads[static_cast<size_t>(t.load_beg + k)];
+                        if (l.slot != k || S + l.ext > g.sp.H) ok = false;
+                    }
+                    const WindowReads wr = window_reads(ps, t);
+                    const int ob = ps.pstep_offs[static_cast<size_t>(t.step_beg)];
+                    for (size_t i = 0; i < wr.term_window.size(); ++i) {
+                        unsigned v = 0;
+                        for (int k = 0; k < 4; ++k) {
+                            const int win = wr.term_window[i][static_cast<size_t>(k)];
+                            v |= static_cast<unsigned>(win < 0 ? 0xff : win) << (8 * k);
+                        }
+                        wslots[static_cast<size_t>(ob) + i] = static_cast<int>(v);
+                    }
+                    for (int k = 0; k < t.store_cnt; ++k)
+                        if (wr.store_window[static_cast<size_t>(k)] >= 0)
+                            wstores[static_cast<size_t>(t.store_beg + k)].y |= 1 << 30;
+                }
+                if (ok) {
+                    o.kwslots = put(wslots.data(), wslots.size() * sizeof(int));
+                    o.kwstores = put(wstores.data(), wstores.size() * sizeof(int2));
+                    o.ktma = true;
+                }
+            }
             // u16 pair mode root band: the second-buffer variant for the
             // double-buffered kernel (load-space slots s < load_cnt -> s + delta)
             const bool last = o_passes.size() + 1 == sp.passes.size();
@@ -446,12 +534,16 @@ void upload(Group& g) {
                         }
                         const int ob = ps.pstep_offs[static_cast<size_t>(t.step_beg)];
                         const int oe = ps.pstep_offs[static_cast<size_t>(t.step_beg + t.nsteps)];
+                        const WindowReads wr = window_reads(ps, t);
+                        for (int sw : wr.store_window)
+                            if (sw >= 0) ok = false;  // a stored window (copy tile): not in the root band
                         for (int oi = ob; oi < oe; ++oi) {
                             const auto& op = ps.pops[static_cast<size_t>(oi)];
                             int4* rec[2] = {&tb[2 * static_cast<size_t>(oi)], &tb1[2 * static_cast<size_t>(oi)]};
                             for (int k = 0; k < op.nterms; ++k) {
-                                if (op.term[k].slot >= t.load_cnt) continue;  // an intermediate column
-                                const int add = 4 * delta_of[static_cast<size_t>(op.term[k].slot)];
+                                const int win = wr.term_window[static_cast<size_t>(oi - ob)][static_cast<size_t>(k)];
+                                if (win < 0) continue;  // an intermediate column
+                                const int add = 4 * delta_of[static_cast<size_t>(win)];
                                 for (int4* r : rec) {
                                     int& f = k == 0 ? r[0].w : k == 1 ? r[1].x : k == 2 ? r[1].y : r[1].z;
                                     f += add;
@@ -497,6 +589,9 @@ void upload(Group& g) {
         d.twin = o.tma ? reinterpret_cast<const int4*>(base + o.twin) : nullptr;
         d.tbops = o.tma ? reinterpret_cast<const int4*>(base + o.tbops) : nullptr;
         d.tbops1 = o.tma ? reinterpret_cast<const int4*>(base + o.tbops1) : nullptr;
+        d.ktma = o.ktma ? 1 : 0;
+        d.kwslots = o.ktma ? reinterpret_cast<const int*>(base + o.kwslots) : nullptr;
+        d.kwstores = o.ktma ? reinterpret_cast<const int2*>(base + o.kwstores) : nullptr;
         d.tile_nc_max = 0;
         for (const auto& t : program(sp.passes[i], g.pairs).tiles) d.tile_nc_max = std::max(d.tile_nc_max, t.store_cnt);
         d.S = g.pass_S[i];
@@ -618,6 +713,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             tw = std::max(1, tw / 2);
         }
         g->pm_D = pm ? pmD : 0;
+        g->acc_sz = acc_sz;
         g->qs.n = static_cast<int>(codes.size());
         for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
         g->ld = round_up(H, acc_sz == 8 ? 16 : 32);
@@ -1049,7 +1145,10 @@ int fht_plan_describe(fht_plan_t plan, char* buf, size_t len) {
             o << "],\"ld\":" << g.ld << ",\"S\":" << g.S << ",\"sr\":" << g.sr << ",\"nbuf\":" << g.nbuf
               << ",\"level_pairs\":" << (g.pairs ? "true" : "false") << ",\"stage_pitch\":" << g.stage_pitch
               << ",\"stage_bytes\":" << g.stage_img << ",\"u16_pair_D\":" << g.pm_D
-              << ",\"k2_tma_windows\":" << ((!g.dt.passes.empty() && g.dt.passes.back().tma) ? "true" : "false")
+              << ",\"k2_tma_windows\":"
+              << (std::any_of(g.dt.passes.begin(), g.dt.passes.end(), [&](const fhtb::PassDev& d) {
+                     return d.tma || (d.ktma && !g.pm_D);
+                 }) ? "true" : "false")
               << ",\"pass_rows\":[";
             for (size_t k = 0; k < g.dt.passes.size(); ++k)
                 o << (k ? "," : "") << "[" << g.dt.passes[k].S << "," << g.dt.passes[k].L << "]";

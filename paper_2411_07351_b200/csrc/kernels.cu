@@ -191,6 +191,13 @@ __device__ __forceinline__ void rows_op(uint32_t d, uint32_t a, uint32_t bb, int
     }
 }
 
+// TMA windows in k2_pass: the residue (in bytes) of window w, two bits per
+// window in two 64-bit masks
+__device__ __forceinline__ uint32_t win_adj(unsigned long long m0, unsigned long long m1, unsigned w) {
+    const unsigned long long m = (w & 32) ? m1 : m0;
+    return static_cast<uint32_t>((m >> (2 * (w & 31))) & 3ull) << 2;
+}
+
 __device__ __forceinline__ int lds1u(uint32_t a) {
     int v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -457,15 +464,24 @@ __device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __rest
     }
 }
 
-template <class Acc, int NWARPS, bool DIRECT>
+template <class Acc, int NWARPS, bool DIRECT, bool WADJ = false>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
-                                               int rows_out = 0) {
+                                               int rows_out = 0, const int* __restrict__ wsl = nullptr,
+                                               unsigned long long m0 = 0, unsigned long long m1 = 0) {
     for (int o = o_beg + warp; o < o_end; o += NWARPS) {
         const int4 h = ops[2 * o], q = ops[2 * o + 1];
         const uint32_t d = base + static_cast<uint32_t>(h.x);
-        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
-                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                         base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        if constexpr (WADJ) {  // terms reading a TMA window: + its alignment residue
+            const unsigned ws = static_cast<unsigned>(wsl[o]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned w = (ws >> (8 * k)) & 0xffu;
+                if (w != 0xffu) t[k] += win_adj(m0, m1, w);
+            }
+        }
         const int n = h.y, nt = h.z & 7, gc = (h.z >> 3) - 1;
         if (DIRECT && gdst != nullptr && gc >= 0) {  // a stored column (non-root band): straight to the workspace
             Acc* __restrict__ g = gdst + (size_t)gc * ld;
@@ -1549,6 +1565,47 @@ __device__ __forceinline__ void issue_windows(const PassDev& ps, const PassTileD
 }
 
 
+// TMA windows for k2_pass (PassDev::ktma): the device form of capi.cu
+// window_copy for the row tile at s0 -- each window placed at word `delta`
+// of its slot so that its long piece is one 16-byte aligned bulk copy; the
+// rest by 4-byte cp.async.  The residues go to two 64-bit shared masks (2
+// bits per window); the ops add them to the terms that read a window.
+__device__ __forceinline__ void issue_windows_dyn(const PassDev& ps, const PassTileDev& tile, const int* __restrict__ in,
+                                                  uint32_t stage, int L, int S, int s0, int H, int ld, int warp,
+                                                  int lane, uint32_t bar, unsigned long long* smask) {
+    constexpr int kW = kThreads2 / 32;
+    for (int w = warp; w < tile.load_cnt; w += kW) {
+        const int4 l = ps.loads[tile.load_beg + w];  // gcol, slot (= w), off, ext
+        const int* __restrict__ col = in + (size_t)l.x * ld;
+        const uint32_t d = stage + static_cast<uint32_t>(l.y) * L * 4u;
+        const int start = wrap_any(s0 + l.z, H), n = S + l.w;
+        int delta, bsrc = 0, bdst = 0, bw = 0, ssrc = 0, sdst = 0, sn = 0;
+        if (start + n <= H) {
+            delta = start & 3;
+            bsrc = start - delta;
+            bw = (n + delta + 3) & ~3;
+        } else {
+            const int a = H - start, b = n - a, c1 = max(0, (H & ~3) - start);
+            if (n - c1 <= a) {
+                delta = start & 3;
+                if (c1 > 0) bsrc = start - delta, bw = c1 + delta;
+                ssrc = start + c1, sdst = delta + c1, sn = n - c1;
+            } else {
+                delta = (4 - (a & 3)) & 3;
+                bdst = delta + a, bw = (b + 3) & ~3;
+                ssrc = start, sdst = delta, sn = a;
+            }
+        }
+        if (lane == 0) {
+            if (bw > 0) bulk_copy(d + 4u * bdst, col + bsrc, 4u * bw, bar);
+            if (delta) atomicOr(smask + (w >> 5), static_cast<unsigned long long>(delta) << (2 * (w & 31)));
+        }
+        uint32_t dd = d + 4u * (sdst + lane);
+        int sw = ssrc + lane;
+        for (int i = lane; i < sn; i += 32, dd += 128u, sw += 32) cp_async4(dd, col + (sw >= H ? sw - H : sw));
+    }
+}
+
 // MODE 0: one level per step, 4 rows per lane; 1: rows interleaved over
 // lanes; 2: level-pair programs (4-byte accumulators only); 4: level pairs of
 // a non-root band, its last step storing the band's columns from registers.
@@ -1620,7 +1677,7 @@ __device__ __forceinline__ void store_root_rows16(Out* __restrict__ o, int W, in
     }
 }
 
-template <class Acc, class Out, int MODE>
+template <class Acc, class Out, int MODE, bool TMAW = false>
 __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* __restrict__ src,
                                                      Acc* __restrict__ dst, long long slot_elems, int W, int H,
                                                      int ld, bool final_pass, OutDesc out, QuadSet qs, int img0,
@@ -1641,13 +1698,24 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     // before the wrap point, 4-byte after); issued first so that the op
     // staging below overlaps their flight.  The bulk-copy mbarrier sits in
     // the gap after the slots; one arrival per warp.
-    const uint32_t bar = (sizeof(Acc) == 4 && ps.bulk) ? smem_u32(sm + (size_t)ps.max_slots * L + 8) : 0u;
+    const uint32_t bar = (sizeof(Acc) == 4 && (ps.bulk || TMAW)) ? smem_u32(sm + (size_t)ps.max_slots * L + 8) : 0u;
+    // TMAW: the windows' alignment residues, two 64-bit masks after the mbarrier
+    unsigned long long* smask = reinterpret_cast<unsigned long long*>(sm + (size_t)ps.max_slots * L + 10);
     if constexpr (sizeof(Acc) == 4) {
         if (bar) {
-            if (tid == 0) mbar_init(bar, kWarps);
+            if (tid == 0) {
+                mbar_init(bar, kWarps);
+                smask[0] = 0ull;
+                smask[1] = 0ull;
+            }
             __syncthreads();
         }
-        issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane, bar);
+        if constexpr (TMAW) {
+            issue_windows_dyn(ps, tile, reinterpret_cast<const int*>(in), smem_u32(sm), L, S, s0, H, ld, warp, lane,
+                              bar, smask);
+        } else {
+            issue_windows<Acc>(ps, tile, in, smem_u32(sm), L, S, s0, H, ld, warp, lane, bar);
+        }
         cp_async_commit();
         if (bar) {
             __syncwarp();
@@ -1660,8 +1728,11 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     int* ssteps = reinterpret_cast<int*>(sops + ps.max_tile_ops);  // the tile's step offsets (after the ops)
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid];
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
+    int* swsl = ssteps + 64;  // TMAW: per op, the window each term reads
     if constexpr (MODE == 2 || MODE == 4 || MODE == 6) {
         for (int k = tid; k < 2 * nops; k += kThreads2) sbops[k] = ps.bops[2 * op0 + k];
+        if constexpr (TMAW)
+            for (int k = tid; k < nops; k += kThreads2) swsl[k] = ps.kwslots[op0 + k];
     } else if constexpr (sizeof(Acc) == 4) {
         for (int k = tid; k < nops; k += kThreads2) sbops[k] = ps.bops[op0 + k];
     } else {
@@ -1681,11 +1752,15 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     }
     // 2. merge levels
     const uint32_t sbase = smem_u32(sm);
+    unsigned long long m0 = 0, m1 = 0;  // TMAW: the windows' residues (read after the first barrier)
     for (int k = 0; k < tile.nsteps; ++k) {
         __syncthreads();
+        if constexpr (TMAW) {
+            if (k == 0) m0 = smask[0], m1 = smask[1];
+        }
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
         if constexpr (MODE == 2) {
-            run_step_terms<Acc, kWarps, false>(sbase, sbops, ob, oe, warp, lane);
+            run_step_terms<Acc, kWarps, false, TMAW>(sbase, sbops, ob, oe, warp, lane, nullptr, 0, 0, swsl, m0, m1);
         } else if constexpr (MODE == 6) {
             // u16 pair mode: the root step widens the packed halves to 32 bits
             if (k + 1 < tile.nsteps) run_step_terms<Acc, kWarps, false>(sbase, sbops, ob, oe, warp, lane);
@@ -1693,9 +1768,9 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
         } else if constexpr (MODE == 4) {
             // the last step of a non-root band stores its columns from registers
             const bool direct = k + 1 == tile.nsteps;
-            run_step_terms<Acc, kWarps, true>(sbase, sbops, ob, oe, warp, lane,
-                                              direct ? dst + (size_t)slot * slot_elems + s0 : nullptr, ld,
-                                              min(S, H - s0));
+            run_step_terms<Acc, kWarps, true, TMAW>(sbase, sbops, ob, oe, warp, lane,
+                                                    direct ? dst + (size_t)slot * slot_elems + s0 : nullptr, ld,
+                                                    min(S, H - s0), swsl, m0, m1);
         }
         else if constexpr (sizeof(Acc) == 4)
             run_step_baked<Acc, kWarps, MODE == 1>(sbase, sbops, ob, oe, warp, lane);
@@ -1711,13 +1786,26 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
     if (!final_pass) {
         Acc* __restrict__ o = dst + (size_t)slot * slot_elems;
         const bool al = ((ld | s0) & 3) == 0;
+        if constexpr (TMAW) {
+            if (tile.nsteps == 0) m0 = smask[0], m1 = smask[1];
+        }
         for (int cb = 0; cb < tile.store_cnt; cb += 32 * kWarps) {
             const int mine = cb + warp + kWarps * lane;
-            const int2 rec = mine < tile.store_cnt ? ps.stores[tile.store_beg + mine] : make_int2(0, 0);
+            const int2 rec = mine < tile.store_cnt ? (TMAW ? ps.kwstores : ps.stores)[tile.store_beg + mine]
+                                                   : make_int2(0, 0);
             const int cnt = min(32, (tile.store_cnt - cb - warp + kWarps - 1) / kWarps);
             for (int j = 0; j < cnt; ++j) {
-                const int sl = __shfl_sync(0xffffffffu, rec.x, j), gc = __shfl_sync(0xffffffffu, rec.y, j);
-                warp_store_col<Acc, Acc>(o + (size_t)gc * ld + s0, sm + (size_t)sl * L, rows, al, lane);
+                const int sl = __shfl_sync(0xffffffffu, rec.x, j);
+                int gc = __shfl_sync(0xffffffffu, rec.y, j);
+                const Acc* sv = sm + (size_t)sl * L;
+                if constexpr (TMAW) {  // a stored window (copy tile): at its alignment residue
+                    if (gc & (1 << 30)) {
+                        gc &= ~(1 << 30);
+                        sv += win_adj(m0, m1, static_cast<unsigned>(sl)) >> 2;
+                    }
+                }
+                // (a shifted window start is not 16-byte aligned: the store takes its scalar path)
+                warp_store_col<Acc, Acc>(o + (size_t)gc * ld + s0, sv, rows, al && (sv - sm) % 4 == 0, lane);
             }
         }
     } else {
@@ -2143,9 +2231,17 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                 continue;
             }
         }
+        size_t smem2t = smem2;
+        if constexpr (sizeof(Acc) == 4) {
+            // level-pair bands (not the pair mode's): windows by the TMA engine
+            if (ps.pairs && ps.ktma && !g.pm_D && !g.k2_bulk) {
+                k2 = final_pass ? k2_pass<Acc, Out, 2, true> : k2_pass<Acc, Out, 4, true>;
+                smem2t += static_cast<size_t>(ps.max_tile_ops) * sizeof(int);  // the ops' window indices
+            }
+        }
         allow_smem(reinterpret_cast<const void*>(k2));
         dim3 g2(((g.pm_D ? g.pm_D : g.H) + ps.S - 1) / ps.S, ps.ntiles, nslots);
-        launch_k(g.pdl, k2, g2, dim3(kThreads2), smem2, st, pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out,
+        launch_k(g.pdl, k2, g2, dim3(kThreads2), smem2t, st, pd, SRC, DST, slot_elems, g.W, g.H, g.ld, final_pass, g.out,
                  g.qs, g.img0, g.pm_D);
         ++launches;
         if (hook) hook(ctx, final_pass ? 3 : 2);

@@ -77,6 +77,12 @@ struct PassDev {
     const int4* twin;
     const int4* tbops;
     const int4* tbops1;
+    // TMA windows in k2_pass (ktma = 1; level-pair programs, 4-byte
+    // accumulators): per op the window index each term reads (4 x u8, 0xff
+    // none); the stores with bit 30 of the column set read a window
+    int ktma;
+    const int* kwslots;
+    const int2* kwstores;
 };
 
 struct GroupLaunch {

@@ -360,3 +360,19 @@ def test_profiled_launch_accounting(monkeypatch):
     pitch = plan.describe()["groups"][0]["stage_pitch"]
     assert pitch % 16 == 0 and pitch >= n + 31
     assert b[0] == 3 * (cells + 2 * n * pitch)  # image read + both staged column sets written
+
+
+@pytest.mark.parametrize("h,w,dt", [(300, 777, "f32"), (1000, 1000, "u8"), (96, 3001, "f32"), (513, 130, "i32")])
+def test_tma_band_windows_option(monkeypatch, h, w, dt):
+    """FHT_K2_TMA_BANDS=1: the level-pair bands' windows by the TMA engine,
+    alignment residues applied per row tile at run time -- bit-exact."""
+    rng = np.random.default_rng(h + w)
+    img = (rng.standard_normal((h, w)).astype(np.float32) if dt == "f32"
+           else rng.integers(0, 200, (h, w)).astype(np.uint8 if dt == "u8" else np.int32))
+    acc = "f32" if dt == "f32" else "i32"
+    monkeypatch.setenv("FHT_K2_TMA_BANDS", "1")
+    out, plan = run_plan(img, dt, acc)
+    assert any(g["k2_tma_windows"] for g in plan.describe()["groups"])
+    ref, _ = oracle.fht2d_quadrants(img, 1, dtype=np.float32 if dt == "f32" else np.int32)
+    for k in Q:
+        np.testing.assert_array_equal(out[k][0], ref[k])
