@@ -194,10 +194,15 @@ def cpu_baseline(cfg: str, strategy: int, seconds: float, threads: int | None = 
             break
     dt = time.perf_counter() - t0
     sums = len(quads) * done * c.n * c.n * int(np.ceil(np.log2(c.n)))
-    used = min(threads, per * len(quads))  # work items are (image, quadrant) pairs
+    # work items (oracle/ref_shim.cpp ref_batch_quadrants_u8): whole images through the
+    # reference's fht2d_quadrants when there are at least as many images as threads,
+    # else (image, quadrant) pairs
+    per_image = mask == 15 and per >= threads
+    used = min(threads, per if per_image else per * len(quads))
+    items = "images (fht::fht2d_quadrants each)" if per_image else "(image, quadrant) items"
     return {"value": sums / dt / 1e9, "unit": "Gsums/s", "cores": used, "kind": kind, "cpu_model": cpu_model(),
             "sample": f"{done} image(s) of {cfg} ({c.n}x{c.n}, {len(quads)} quadrant(s)){proxy}, "
-                      f"{dt:.2f} s, (image, quadrant) items over {used} host thread(s)"}
+                      f"{dt:.2f} s, {items} over {used} host thread(s)"}
 
 
 def cpu_single_thread(cfg: str, strategy: int, seconds: float):

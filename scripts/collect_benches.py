@@ -20,8 +20,11 @@ for c in cfgs:
         lsu = tj.get("lsu_issue", {}).get(c, {}).get(k)
         if lsu:
             r["lsu_pipe_frac_ncu"], r["issue_frac_ncu"] = lsu
+            r["lsu_floor_ms"] = round(lsu[0] * r["avg_launch_ms"], 4)
+            r["frac_at_lsu_floor"] = round(r["achieved"] / lsu[0] / r["peak"], 4)
         else:
-            r.pop("lsu_pipe_frac_ncu", None), r.pop("issue_frac_ncu", None)
+            for k in ("lsu_pipe_frac_ncu", "issue_frac_ncu", "lsu_floor_ms", "frac_at_lsu_floor"):
+                r.pop(k, None)
     (ROOT / "profiles" / f"{rnd}_bench_{c}.json").write_text(json.dumps(d) + "\n")
     print(c, d["value"], r and (r["kernel"], r["frac"], r["traffic"]))
 ref = src / "bench_reference_c4.json"

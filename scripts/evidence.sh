@@ -1,6 +1,7 @@
 #!/bin/bash
-# One GPU-box evidence run: benches, reference arm, ncu launch list and full
-# captures.  Outputs under gpurun_out/ev/.
+# One GPU-box evidence run: benches (c4 default + c1/c2/c3/c5), the reference
+# arm, the ncu launch list of the c4 bench command and full captures of the
+# c4 and c5 kernels.  Outputs under gpurun_out/ev/.
 set -u
 O=gpurun_out/ev; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.csv 2>&1

@@ -22,9 +22,12 @@ cols = ["Warp Stall Sampling (All Samples)", "Instructions Executed", "L1 Wavefr
         "L1 Wavefronts Shared Excessive", "L1 Tag Requests Global"]
 ix = {k: h.index(k) for k in cols + ["Source"]}
 agg = defaultdict(lambda: [0.0] * len(cols))
+seen = set()  # the source page repeats every SASS line (once per view): count each address once
+ia = h.index("Address")
 for r in rows[1:]:
-    if len(r) < len(h):
+    if len(r) < len(h) or r[ia] in seen:
         continue
+    seen.add(r[ia])
     s = re.sub(r"^@!?U?P\w+\s+", "", r[ix["Source"]].strip())
     op = s.split()[0] if s else "?"
     for j, k in enumerate(cols):

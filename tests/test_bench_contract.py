@@ -30,7 +30,7 @@ def test_reference_arm_line():
 
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
 def test_committed_bench_lines(cfg):
-    path = ROOT / "profiles" / f"r01_bench_{cfg}.json"
+    path = ROOT / "profiles" / f"r02_bench_{cfg}.json"
     line = json.loads(path.read_text().strip().splitlines()[-1])
     assert BASE_KEYS <= set(line)
     assert line["config"]["workload"] == cfg and "l2" in line["config"]
@@ -48,7 +48,11 @@ def test_committed_bench_lines(cfg):
     e = line["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and 0 < e["value"] < line["value"]
     cb = line["cpu_baseline"]
-    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] > 0
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] > 0 and cb["cpu_model"]
+    st = cb["single_thread"]  # the reference as it runs: one thread
+    assert st["cores"] == 1 and 0 < st["value"] < cb["value"] and st["kind"] == "reference"
+    if "lsu_pipe_frac_ncu" in r:  # the LSU floor explains the HBM fraction
+        assert r["lsu_floor_ms"] == pytest.approx(r["lsu_pipe_frac_ncu"] * r["avg_launch_ms"], rel=1e-2)
     c = line["clocks"]
     assert not set(c["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     assert c["sm_mhz"] >= 0.9 * c["sm_max_mhz"]
