@@ -12,9 +12,20 @@ import sys
 from collections import defaultdict
 
 rep, kern = sys.argv[1], sys.argv[2]
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kern}"],
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:k"],
                      capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(src)))
+# the page holds one block per kernel (each starting with a "Kernel Name" line);
+# keep the first block whose name contains `kern`
+keep, lines = False, []
+for line in src.splitlines():
+    if line.startswith('"Kernel Name"'):
+        if keep:
+            break
+        keep = kern in line
+        continue
+    if keep:
+        lines.append(line)
+rows = list(csv.reader(io.StringIO("\n".join(lines))))
 while rows and "Source" not in rows[0]:
     rows = rows[1:]
 h = rows[0]
