@@ -229,6 +229,12 @@ int fht_schedule_json(int W, int H, int strategy, int block_width, int pass_leve
 int fht_plan_cache_clear(size_t* released);
 size_t fht_plan_cache_size(void);
 
+/* Diagnostics: the stream synchronisations and device allocations this
+ * library has made so far (process-wide).  Lets a test check that a timed
+ * step -- an execute, or the multi-GPU root split's child + merge -- makes
+ * neither. */
+int fht_debug_counters(uint64_t* host_syncs, uint64_t* device_allocs);
+
 /* Message of the last failed call on this thread ("" if none). */
 const char* fht_last_error(void);
 

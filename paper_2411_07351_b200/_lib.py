@@ -58,6 +58,7 @@ SIGNATURES = {
     "fht_schedule_json": (_i, [_i, _i, _i, _i, _i, _i, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "fht_plan_cache_clear": (_i, [ctypes.POINTER(ctypes.c_size_t)]),
     "fht_plan_cache_size": (ctypes.c_size_t, []),
+    "fht_debug_counters": (_i, [_pu64, _pu64]),
     "fht_last_error": (ctypes.c_char_p, []),
     "fht_version": (ctypes.c_char_p, []),
 }
@@ -95,6 +96,13 @@ def lib() -> ctypes.CDLL:
             f.argtypes = args
         _lib = l
     return _lib
+
+
+def debug_counters() -> tuple[int, int]:
+    """(stream synchronisations, device allocations) the library has made so far."""
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib().fht_debug_counters(ctypes.byref(a), ctypes.byref(b)))
+    return int(a.value), int(b.value)
 
 
 def check(rc: int) -> None:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -34,6 +35,24 @@ struct FhtError : std::runtime_error {
     int code;
     FhtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
+
+// Host synchronisations and device allocations the library makes (for the
+// tests that check a timed step does neither: fht_debug_counters).
+std::atomic<unsigned long long> g_host_syncs{0}, g_device_allocs{0};
+cudaError_t counted_sync(cudaStream_t s) {
+    g_host_syncs.fetch_add(1, std::memory_order_relaxed);
+    return cudaStreamSynchronize(s);
+}
+template <class T>
+cudaError_t counted_malloc(T** p, size_t n) {
+    g_device_allocs.fetch_add(1, std::memory_order_relaxed);
+    return cudaMalloc(p, n);
+}
+template <class T>
+cudaError_t counted_malloc_async(T** p, size_t n, cudaStream_t s) {
+    g_device_allocs.fetch_add(1, std::memory_order_relaxed);
+    return cudaMallocAsync(p, n, s);
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw FhtError(FHT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -563,7 +582,7 @@ void upload(Group& g) {
         o_passes.push_back(o);
     }
     blob.resize(blob.size() + 16);
-    cuda_check(cudaMalloc(&g.dt.blob, blob.size()), "cudaMalloc(plan tables)");
+    cuda_check(counted_malloc(&g.dt.blob, blob.size()), "counted_malloc(plan tables)");
     cuda_check(cudaMemcpy(g.dt.blob, blob.data(), blob.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan tables)");
     char* base = static_cast<char*>(g.dt.blob);
     g.dt.blocks = reinterpret_cast<const int4*>(base + o_blocks);
@@ -916,11 +935,11 @@ void execute_host(fht_plan_s* p, const void* h_in, void* const h_out[4], cudaStr
     const int per_part = (p->batch + nparts - 1) / nparts;
     const size_t ws_per_img = p->chunk ? p->ws_bytes / static_cast<size_t>(p->chunk) : 0;
     const size_t ws_part = ws_per_img * static_cast<size_t>(std::min(per_part, p->chunk));
-    if (!p->st_in) cuda_check(cudaMalloc(&p->st_in, in_img * p->batch), "cudaMalloc(staging in)");
+    if (!p->st_in) cuda_check(counted_malloc(&p->st_in, in_img * p->batch), "counted_malloc(staging in)");
     for (int q = 0; q < 4; ++q)
         if ((p->mask & (1 << q)) && !p->st_out[q])
-            cuda_check(cudaMalloc(&p->st_out[q], out_img * p->batch), "cudaMalloc(staging out)");
-    if (ws_part && !p->st_ws) cuda_check(cudaMalloc(&p->st_ws, ws_part * nst), "cudaMalloc(workspace)");
+            cuda_check(counted_malloc(&p->st_out[q], out_img * p->batch), "counted_malloc(staging out)");
+    if (ws_part && !p->st_ws) cuda_check(counted_malloc(&p->st_ws, ws_part * nst), "counted_malloc(workspace)");
     if (nst > 1 && !p->hst[0]) {
         for (int k = 0; k < kHostStreams; ++k) {
             cuda_check(cudaStreamCreateWithFlags(&p->hst[k], cudaStreamNonBlocking), "cudaStreamCreate");
@@ -953,7 +972,7 @@ void execute_host(fht_plan_s* p, const void* h_in, void* const h_out[4], cudaStr
             cuda_check(cudaStreamWaitEvent(st, p->hev[k], 0), "cudaStreamWaitEvent");
         }
     }
-    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    cuda_check(counted_sync(st), "cudaStreamSynchronize");
 }
 
 // absmax on device -> (ok_for_i32, within 2^62 budget)
@@ -964,13 +983,13 @@ void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok
     }
     if (dtype == FHT_F32) throw std::invalid_argument("check_budget: integer inputs only");
     unsigned long long* d_max = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_max), sizeof(unsigned long long), st), "cudaMallocAsync");
+    cuda_check(counted_malloc_async(reinterpret_cast<void**>(&d_max), sizeof(unsigned long long), st), "cudaMallocAsync");
     cuda_check(cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
     fhtb::launch_absmax(d_in, dtype, count, d_max, st);
     unsigned long long vmax = 0;
     cuda_check(cudaMemcpyAsync(&vmax, d_max, sizeof(vmax), cudaMemcpyDeviceToHost, st), "D2H(absmax)");
     cuda_check(cudaFreeAsync(d_max, st), "cudaFreeAsync");
-    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    cuda_check(counted_sync(st), "cudaStreamSynchronize");
     const unsigned __int128 prod = static_cast<unsigned __int128>(static_cast<unsigned>(width)) * vmax;
     if (prod >= (static_cast<unsigned __int128>(1) << 62))
         throw std::overflow_error("fht2d: width * max|value| reaches 2^62; sums could overflow 64-bit accumulators");
@@ -1044,7 +1063,7 @@ const int4* merge_root_table(int width, int height, int strategy) {
         ops[static_cast<size_t>(t)] = make_int4(t, t0, t1, (t - t1) % height);
     }
     int4* d_ops = nullptr;
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&d_ops), ops.size() * sizeof(int4)), "cudaMalloc(merge table)");
+    cuda_check(counted_malloc(reinterpret_cast<void**>(&d_ops), ops.size() * sizeof(int4)), "counted_malloc(merge table)");
     cuda_check(cudaMemcpy(d_ops, ops.data(), ops.size() * sizeof(int4), cudaMemcpyHostToDevice), "H2D(merge table)");
     tables->emplace(key, d_ops);
     return d_ops;
@@ -1082,10 +1101,10 @@ void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* 
         for (void* q : d_out)
             if (q) cudaFreeAsync(q, st);
         if (d_ws) cudaFreeAsync(d_ws, st);
-        cudaStreamSynchronize(st);
+        counted_sync(st);
     };
     try {
-        cuda_check(cudaMallocAsync(&d_in, cells * 8, st), "cudaMallocAsync(in)");
+        cuda_check(counted_malloc_async(&d_in, cells * 8, st), "counted_malloc_async(in)");
         cuda_check(cudaMemcpyAsync(d_in, img, cells * 8, cudaMemcpyHostToDevice, st), "H2D");
         // check_overflow_budget (transform.cpp:16-27) for every quadrant's working width.
         int ok32 = 0;
@@ -1094,12 +1113,12 @@ void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* 
         const std::shared_ptr<fht_plan_s> sp = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev);
         fht_plan_s* p = sp.get();
         for (int q = 0; q < 4; ++q)
-            if (mask & (1 << q)) cuda_check(cudaMallocAsync(&d_out[q], cells * 8, st), "cudaMallocAsync(out)");
-        if (p->ws_bytes) cuda_check(cudaMallocAsync(&d_ws, p->ws_bytes, st), "cudaMallocAsync(ws)");
+            if (mask & (1 << q)) cuda_check(counted_malloc_async(&d_out[q], cells * 8, st), "counted_malloc_async(out)");
+        if (p->ws_bytes) cuda_check(counted_malloc_async(&d_ws, p->ws_bytes, st), "counted_malloc_async(ws)");
         execute(p, d_in, static_cast<int64_t>(cells), d_out, static_cast<int64_t>(cells), d_ws, st);
         for (int q = 0; q < 4; ++q)
             if (mask & (1 << q)) cuda_check(cudaMemcpyAsync(outs[q], d_out[q], cells * 8, cudaMemcpyDeviceToHost, st), "D2H");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        cuda_check(counted_sync(st), "cudaStreamSynchronize");
         if (adds) *adds = p->additions;
     } catch (...) {
         release();
@@ -1196,7 +1215,7 @@ int fht_execute_profiled(fht_plan_t plan, const void* d_in, int64_t in_image_str
         c.ev.push_back(e0);
         c.kind.push_back(0);
         execute(plan, d_in, in_image_stride, d_out, out_image_stride, d_workspace, c.st, hook, &c);
-        cuda_check(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+        cuda_check(counted_sync(c.st), "cudaStreamSynchronize");
         const int n = static_cast<int>(c.ev.size()) - 1;
         if (n_launches) *n_launches = n;
         // Algorithmic bytes of each launch (every distinct input
@@ -1274,7 +1293,7 @@ int fht_device_alloc(size_t bytes, int device, void** d_ptr) {
     return guarded([&] {
         if (!d_ptr) throw std::invalid_argument("fht_device_alloc: null pointer");
         DeviceGuard dg(device);
-        cuda_check(cudaMalloc(d_ptr, std::max<size_t>(bytes, 1)), "cudaMalloc");
+        cuda_check(counted_malloc(d_ptr, std::max<size_t>(bytes, 1)), "cudaMalloc");
     });
 }
 
@@ -1374,15 +1393,15 @@ int fht_slow_hough_device(const void* d_img, int in_dtype, int width, int height
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         int* d_pat = nullptr;
         long long* d_cols = nullptr;
-        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_pat), pat.size() * sizeof(int), st), "cudaMallocAsync");
-        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_cols), static_cast<size_t>(W) * H * 8, st), "cudaMallocAsync");
+        cuda_check(counted_malloc_async(reinterpret_cast<void**>(&d_pat), pat.size() * sizeof(int), st), "cudaMallocAsync");
+        cuda_check(counted_malloc_async(reinterpret_cast<void**>(&d_cols), static_cast<size_t>(W) * H * 8, st), "cudaMallocAsync");
         cuda_check(cudaMemcpyAsync(d_pat, pat.data(), pat.size() * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
         fhtb::launch_slow_hough(d_img, in_dtype, width, height, quadrant, d_pat, W, H, d_cols,
                                 reinterpret_cast<long long*>(d_hough), st);
         cuda_check(cudaGetLastError(), "slow_hough launch");
         cuda_check(cudaFreeAsync(d_pat, st), "cudaFreeAsync");
         cuda_check(cudaFreeAsync(d_cols, st), "cudaFreeAsync");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");  // the host pattern table goes out of scope
+        cuda_check(counted_sync(st), "cudaStreamSynchronize");  // the host pattern table goes out of scope
     });
 }
 
@@ -1393,8 +1412,8 @@ int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, 
         const size_t cells = static_cast<size_t>(width) * height;
         void* d_in = nullptr;
         void* d_out = nullptr;
-        cuda_check(cudaMallocAsync(&d_in, cells * 8, st), "cudaMallocAsync");
-        cuda_check(cudaMallocAsync(&d_out, cells * 8, st), "cudaMallocAsync");
+        cuda_check(counted_malloc_async(&d_in, cells * 8, st), "cudaMallocAsync");
+        cuda_check(counted_malloc_async(&d_out, cells * 8, st), "cudaMallocAsync");
         try {
             cuda_check(cudaMemcpyAsync(d_in, img, cells * 8, cudaMemcpyHostToDevice, st), "H2D");
             check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), width, nullptr, st);  // oracle.cpp:11
@@ -1402,16 +1421,16 @@ int fht_slow_hough_i64(const int64_t* img, int width, int height, int strategy, 
                                                  static_cast<int64_t*>(d_out), st);
             if (rc != FHT_OK) throw FhtError(rc, g_last_error);
             cuda_check(cudaMemcpyAsync(hough, d_out, cells * 8, cudaMemcpyDeviceToHost, st), "D2H");
-            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            cuda_check(counted_sync(st), "cudaStreamSynchronize");
         } catch (...) {
             cudaFreeAsync(d_in, st);
             cudaFreeAsync(d_out, st);
-            cudaStreamSynchronize(st);
+            counted_sync(st);
             throw;
         }
         cudaFreeAsync(d_in, st);
         cudaFreeAsync(d_out, st);
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        cuda_check(counted_sync(st), "cudaStreamSynchronize");
     });
 }
 
@@ -1423,7 +1442,7 @@ int fht_max_deviation_numerators(int n_lo, int n_hi, int strategy, int64_t* wors
         const size_t cnt = static_cast<size_t>(n_hi - n_lo + 1);
         cudaStream_t st = cudaStreamPerThread;
         unsigned long long* d = nullptr;
-        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d), cnt * 8, st), "cudaMallocAsync");
+        cuda_check(counted_malloc_async(reinterpret_cast<void**>(&d), cnt * 8, st), "cudaMallocAsync");
         cuda_check(cudaMemsetAsync(d, 0, cnt * 8, st), "cudaMemsetAsync");
         // slices of widths keep each launch's grid.y and run time bounded
         for (int a = n_lo; a <= n_hi; a += 8192) {
@@ -1433,7 +1452,7 @@ int fht_max_deviation_numerators(int n_lo, int n_hi, int strategy, int64_t* wors
         cuda_check(cudaGetLastError(), "max_deviation launch");
         cuda_check(cudaMemcpyAsync(worst, d, cnt * 8, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaFreeAsync(d, st), "cudaFreeAsync");
-        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        cuda_check(counted_sync(st), "cudaStreamSynchronize");
     });
 }
 
@@ -1546,6 +1565,12 @@ int fht_plan_cache_clear(size_t* released) {
 }
 
 size_t fht_plan_cache_size(void) { return plan_cache_size(); }
+
+int fht_debug_counters(uint64_t* host_syncs, uint64_t* device_allocs) {
+    if (host_syncs) *host_syncs = g_host_syncs.load();
+    if (device_allocs) *device_allocs = g_device_allocs.load();
+    return FHT_OK;
+}
 
 const char* fht_version(void) { return "fht_b200 0.1 (sm_100a)"; }
 

@@ -112,3 +112,25 @@ def test_plan_cache_is_bounded(monkeypatch):
     # still works after a clear
     img = workloads.make_images("c1", 1)[0][:40, :40].astype(np.int64)
     assert np.array_equal(fht.fht2d(img), oracle.fht2d_counted_i64(img)[0])
+
+
+def test_execute_makes_no_host_sync_or_allocation():
+    """fht_execute is stream ordered: no stream synchronisation and no device
+    allocation per call (debug counters of the library, torch's allocator)."""
+    from paper_2411_07351_b200 import _lib
+
+    imgs = workloads.make_images("c4", 8)
+    plan = fht.Plan(509, 509, "tweaked", in_dtype="u8", acc_dtype="i32", batch=8)
+    x = torch.from_numpy(imgs).cuda()
+    out = plan.alloc_outputs()
+    plan(x, out=out)
+    torch.cuda.synchronize()
+    c0, a0 = _lib.debug_counters(), torch.cuda.memory_stats()["allocation.all.allocated"]
+    for _ in range(5):
+        plan(x, out=out)
+    assert _lib.debug_counters() == c0
+    assert torch.cuda.memory_stats()["allocation.all.allocated"] == a0
+    torch.cuda.synchronize()
+    ref, _ = oracle.fht2d_quadrants(imgs[3], oracle.TWEAKED, dtype=np.int32)
+    for q in fht.QUADRANTS:
+        assert np.array_equal(out[q][3].cpu().numpy(), ref[q])

@@ -38,11 +38,19 @@ def _root_worker(rank, port, out, exchange):
     sys.path.insert(0, str(ROOT))
     from paper_2411_07351_b200 import shard
 
+    from paper_2411_07351_b200 import _lib
+
     be = shard.GpuRootBackend("tweaked", "f32", "f32")
+    imgs = [torch.from_numpy(np.random.default_rng(9 + k).random((1500, 2049), dtype=np.float32)).cuda()
+            for k in range(3)]
     for k in range(3):  # three steps, a new image each: buffers, events and counters are reused across steps
-        rng = np.random.default_rng(9 + k)
-        img = torch.from_numpy(rng.random((1500, 2049), dtype=np.float32)).cuda()
-        res, sp = shard.root_split_quadrant(img, "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
+        if k == 1:  # after the first step (plans, buffers, IPC set up): no allocation, no host sync
+            c0 = _lib.debug_counters()
+            a0 = torch.cuda.memory_stats()["allocation.all.allocated"]
+        res, sp = shard.root_split_quadrant(imgs[k], "vert_pos", "tweaked", side=rank, backend=be, peer=1 - rank)
+    if exchange == "p2p":
+        assert _lib.debug_counters() == c0, (c0, _lib.debug_counters())
+        assert torch.cuda.memory_stats()["allocation.all.allocated"] == a0
     torch.cuda.synchronize()
     np.save(f"{out}.{rank}.npy", res.cpu().numpy())
     dist.barrier()
