@@ -335,7 +335,8 @@ __device__ __forceinline__ void rows_op_terms_global(Acc* __restrict__ g, const 
 // rows_op_terms for 256 <= n < 288 (a full 256-row tile plus a halo of < 32
 // rows): 8 whole groups with compile-time offsets, then one lane-predicated
 // group -- no loop control.
-template <class Acc, int K, int SPLIT>
+// (NH = 2: 256 <= n < 288; NH = 1: the same for 128-row tiles, 128 <= n < 160)
+template <class Acc, int K, int SPLIT, int NH = 2>
 __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t)[4], int n, int lane) {
     const uint32_t lo = lane * 4u;
     uint32_t p[4];
@@ -343,7 +344,7 @@ __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t
     for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
     const uint32_t dd = opaque(d + lo);
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
+    for (int half = 0; half < NH; ++half) {
         int v[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -352,23 +353,23 @@ __device__ __forceinline__ void rows_op_terms_256(uint32_t d, const uint32_t (&t
 #pragma unroll
         for (int u = 0; u < 4; ++u) sts1u(dd + 512u * half + 128u * u, sum_terms<Acc, K, SPLIT>(v[u]));
     }
-    if (256 + lane < n) {
+    if (128 * NH + lane < n) {
         int v[4];
 #pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = lds1u(p[k] + 1024u);
-        sts1u(dd + 1024u, sum_terms<Acc, K, SPLIT>(v));
+        for (int k = 0; k < K; ++k) v[k] = lds1u(p[k] + 512u * NH);
+        sts1u(dd + 512u * NH, sum_terms<Acc, K, SPLIT>(v));
     }
 }
 
 // rows_op_terms_global for exactly 256 rows (a full tile): no loop control
-template <class Acc, int K, int SPLIT>
+template <class Acc, int K, int SPLIT, int NH = 2>
 __device__ __forceinline__ void rows_op_terms_global_256(Acc* __restrict__ g, const uint32_t (&t)[4], int lane) {
     const uint32_t lo = lane * 4u;
     uint32_t p[4];
 #pragma unroll
     for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
+    for (int half = 0; half < NH; ++half) {
         int v[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -486,6 +487,7 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
         if (DIRECT && gdst != nullptr && gc >= 0) {  // a stored column (non-root band): straight to the workspace
             Acc* __restrict__ g = gdst + (size_t)gc * ld;
             if (nt == 4 && rows_out == 256) rows_op_terms_global_256<Acc, 4, 2>(g, t, lane);
+            else if (nt == 4 && rows_out == 128) rows_op_terms_global_256<Acc, 4, 2, 1>(g, t, lane);
             else if (nt == 4) rows_op_terms_global<Acc, 4, 2>(g, t, rows_out, lane);
             else if (nt == 2 && rows_out == 256) rows_op_terms_global_256<Acc, 2, 1>(g, t, lane);
             else if (nt == 2) rows_op_terms_global<Acc, 2, 1>(g, t, rows_out, lane);
@@ -497,6 +499,7 @@ __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __rest
         }
         if (nt == 4) {
             if (n >= 256 && n < 288) rows_op_terms_256<Acc, 4, 2>(d, t, n, lane);
+            else if (n >= 128 && n < 160) rows_op_terms_256<Acc, 4, 2, 1>(d, t, n, lane);
             else rows_op_terms<Acc, 4, 2>(d, t, n, lane);
         } else if (nt == 2) {
             if (n >= 256 && n < 288) rows_op_terms_256<Acc, 2, 1>(d, t, n, lane);
