@@ -17,6 +17,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fht_b200.h"
 #include "kernels.cuh"
 #include "plan.hpp"
@@ -848,6 +850,10 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
         if ((p->mask & (1 << q)) && !d_out[q]) throw std::invalid_argument("fht_execute: null output for a selected quadrant");
     if (p->ws_bytes && !ws) throw std::invalid_argument("fht_execute: null workspace");
     DeviceGuard dg(p->device);
+    nvtxRangePushA("fht_execute");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     for (int img0 = img_begin; img0 < img_end; img0 += p->chunk) {
         const int nimg = std::min(p->chunk, img_end - img0);
         for (auto& gp : p->groups) {

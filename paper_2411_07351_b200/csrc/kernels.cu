@@ -25,6 +25,8 @@
 #include <utility>
 #include <type_traits>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.cuh"
 
 namespace fhtb {
@@ -614,6 +616,15 @@ __device__ __forceinline__ void warp_store_col(Out* __restrict__ g, const Acc* s
 // dependent launches of small transforms.  No early trigger: a dependent
 // never holds shared memory a running predecessor still needs.
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// One NVTX range per launch phase (SURVEY §5 tracing): free without a tool
+// attached, named phases on an nsys / ncu timeline with one.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class... KArgs, class... Args>
 void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
@@ -2127,6 +2138,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
             const long long ext_w = std::max<long long>(g.img_w, g.stage_p >= 0 ? g.stage_pitch : 0);
             const long long ext_h = std::max<long long>(g.img_h, g.stage_t >= 0 ? g.stage_pitch : 0);
             dim3 gs(static_cast<unsigned>((ext_w + 63) / 64), static_cast<unsigned>((ext_h + 63) / 64), g.nimg);
+            NvtxRange nr("fht: u8 staging");
             launch_k(g.pdl, k_stage_u8, gs, dim3(256), 0, st, im, g.img_w, g.img_h, g.img_pitch, g.img_stride, g.img0,
                      g.stage, g.stage_img, g.stage_pitch, g.stage_t, g.stage_pitch, g.stage_p);
             ++launches;
@@ -2147,6 +2159,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     };
     if (both) fork_join(g.ev_fork, st, st1);
     if (g.nblocks > 0) {
+        NvtxRange nr("fht: pass 0, generic blocks (K1)");
         dim3 g1(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nblocks, nslots);
         auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;
         allow_smem(reinterpret_cast<const void*>(k1));
@@ -2159,6 +2172,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     }
     if constexpr (sizeof(Acc) == 4) {
         if (g.nby > 0) {
+            NvtxRange nr("fht: pass 0, width-32 blocks (K1P)");
             auto kb = g.k1p_variant == 0   ? k1_by32<In, Acc, 0>
                       : g.k1p_variant == 2 ? k1_by32<In, Acc, 2>
                       : g.k1p_variant == 3 ? k1_by32<In, Acc, 3>
@@ -2196,6 +2210,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
     for (int p = 0; p < g.npasses; ++p) {
         const PassDev& ps = g.passes[p];
         const bool final_pass = (p == g.npasses - 1);
+        NvtxRange nr(final_pass ? "fht: root band (K2)" : "fht: upper band (K2)");
         const Acc* SRC = ws + (size_t)(p & 1) * g.W * g.ld;          // pass p reads buffer (p-1)%2 ... K1 wrote 0
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
