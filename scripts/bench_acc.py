@@ -1,0 +1,44 @@
+"""Device time of one transform per accumulator type (int32 vs int64 vs f32)
+on the same image size: the int64 path (values too large for int32 sums,
+transform.cpp:16-27's budget) against the int32 one.
+
+    python scripts/bench_acc.py --n 1024 --quadrants 4 --batch 1
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2411_07351_b200 import fht  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=1024)
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--iters", type=int, default=20)
+a = ap.parse_args()
+n, b = a.n, a.batch
+sums = 4 * b * n * n * int(np.ceil(np.log2(n)))
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+for in_dt, acc in (("i32", "i32"), ("i64", "i64"), ("i32", "i64"), ("f32", "f32")):
+    tdt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[in_dt]
+    x = (torch.randint(-(1 << 20), 1 << 20, (b, n, n), dtype=torch.int64) if in_dt != "f32"
+         else torch.randn(b, n, n)).to(tdt).cuda()
+    plan = fht.Plan(n, n, "tweaked", in_dtype=in_dt, acc_dtype=acc, batch=b)
+    out = plan.alloc_outputs()
+    for _ in range(3):
+        plan(x, out=out)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(a.iters):
+        flush.fill_(1)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        plan(x, out=out)
+        e.record()
+        torch.cuda.synchronize()
+        ms.append(s.elapsed_time(e))
+    m = float(np.median(ms))
+    print(f"{n}x{n} x{b} in={in_dt} acc={acc}: {m:.4f} ms  {sums / m / 1e6:.1f} Gsums/s  launches {plan.launches}")
