@@ -430,8 +430,9 @@ void upload(Group& g) {
                 for (size_t oi = 0; oi < ps.pops.size(); ++oi) {
                     const auto& op = ps.pops[oi];
                     int64_t t[4] = {0, 0, 0, 0};
-                    for (int k = 0; k < op.nterms; ++k) t[k] = (op.term[k].slot * L + op.term[k].off) * 4;
-                    const int64_t d = op.dst * L * 4;
+                    const int64_t esz = static_cast<int64_t>(g.acc_sz);
+                    for (int k = 0; k < op.nterms; ++k) t[k] = (op.term[k].slot * L + op.term[k].off) * esz;
+                    const int64_t d = op.dst * L * esz;
                     if (d > INT32_MAX || *std::max_element(t, t + 4) > INT32_MAX)
                         throw FhtError(FHT_ERR_INTERNAL, "op offset overflow");
                     if (gcol_of[oi] >= (1 << 27)) throw FhtError(FHT_ERR_INTERNAL, "column index overflow");
@@ -692,7 +693,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         const size_t budget = static_cast<size_t>(env_int("FHT_K2_SMEM_KB", 105, 16, 220)) * 1024;
         const int levels = env_int("FHT_PASS_LEVELS", 5, 1, 8);
         int tw = env_int("FHT_TILE_WIDTH", 32, 1, 64);  // K2's root store handles <= 64 slopes per tile
-        g->pairs = acc_sz == 4 && env_int("FHT_K2_PAIRS", 1, 0, 1) == 1;
+        g->pairs = (acc_sz == 4 || acc_sz == 8) && env_int("FHT_K2_PAIRS", 1, 0, 1) == 1;
         // u16 pair mode: u8 images whose root children are at
         // most 257 wide (every non-root node sum < 2^16) and H <= 512 (one
         // K1P/K2 row tile of D = H/2 rounded up to 8 words).  It needs the

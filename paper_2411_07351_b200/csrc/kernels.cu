@@ -449,6 +449,89 @@ __device__ __forceinline__ void rows_op_widen_256(uint32_t d, uint32_t dh, const
     }
 }
 
+// 8-byte accumulators (int64): the same level-pair ops on 64-bit words --
+// lane l owns rows l, l + 32, ... (256 bytes per 32 rows, two wavefronts).
+__device__ __forceinline__ long long lds2u(uint32_t a) {
+    long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts2u(uint32_t a, long long v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+template <int K, int SPLIT>
+__device__ __forceinline__ long long sum_terms64(const long long (&v)[4]) {
+    if constexpr (K == 2) return v[0] + v[1];
+    if constexpr (K == 3 && SPLIT == 2) return (v[0] + v[1]) + v[2];
+    if constexpr (K == 3) return v[0] + (v[1] + v[2]);
+    return (v[0] + v[1]) + (v[2] + v[3]);
+}
+// d (shared) or g (global, DIRECT) = the op's K shifted windows, rows [0, n)
+template <int K, int SPLIT, bool GLOBAL>
+__device__ __forceinline__ void rows_op_terms64(uint32_t d, long long* __restrict__ g, const uint32_t (&t)[4], int n,
+                                                int lane) {
+    constexpr int U = 4;
+    const uint32_t lo = lane * 8u;
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = opaque(t[k] + lo);
+    const uint32_t dd = opaque(d + lo);
+    int i0 = 0;
+    for (; i0 + 32 * U <= n; i0 += 32 * U) {
+        long long v[U][4];
+        const uint32_t o = i0 * 8u;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[u][k] = lds2u(p[k] + o + 256u * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long r = sum_terms64<K, SPLIT>(v[u]);
+            if constexpr (GLOBAL) g[i0 + 32 * u + lane] = r;
+            else sts2u(dd + o + 256u * u, r);
+        }
+    }
+    for (; i0 < n; i0 += 32)
+        if (i0 + lane < n) {
+            const uint32_t o = i0 * 8u;
+            long long v[4];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = lds2u(p[k] + o);
+            const long long r = sum_terms64<K, SPLIT>(v);
+            if constexpr (GLOBAL) g[i0 + lane] = r;
+            else sts2u(dd + o, r);
+        }
+}
+template <int NWARPS, bool DIRECT>
+__device__ __forceinline__ void run_step_terms64(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
+                                                 int warp, int lane, long long* __restrict__ gdst = nullptr, int ld = 0,
+                                                 int rows_out = 0) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 h = ops[2 * o], q = ops[2 * o + 1];
+        const uint32_t d = base + static_cast<uint32_t>(h.x);
+        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        const int nt = h.z & 7, gc = (h.z >> 3) - 1, sp2 = (q.w & 15) == 2;
+        long long* __restrict__ g = DIRECT && gdst != nullptr && gc >= 0 ? gdst + (size_t)gc * ld : nullptr;
+        const int n = g ? rows_out : h.y;
+        if (g) {  // a stored column (non-root band): straight to the workspace
+            if (nt == 4) rows_op_terms64<4, 2, true>(0u, g, t, n, lane);
+            else if (nt == 2) rows_op_terms64<2, 1, true>(0u, g, t, n, lane);
+            else if (nt == 3 && sp2) rows_op_terms64<3, 2, true>(0u, g, t, n, lane);
+            else if (nt == 3) rows_op_terms64<3, 1, true>(0u, g, t, n, lane);
+            else
+                for (int i = lane; i < n; i += 32) g[i] = lds2u(t[0] + 8u * i);
+            continue;
+        }
+        if (nt == 4) rows_op_terms64<4, 2, false>(d, nullptr, t, n, lane);
+        else if (nt == 2) rows_op_terms64<2, 1, false>(d, nullptr, t, n, lane);
+        else if (nt == 3 && sp2) rows_op_terms64<3, 2, false>(d, nullptr, t, n, lane);
+        else if (nt == 3) rows_op_terms64<3, 1, false>(d, nullptr, t, n, lane);
+        else
+            for (int i = lane; i < n; i += 32) sts2u(d + 8u * i, lds2u(t[0] + 8u * i));
+    }
+}
+
 template <int NWARPS>
 __device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane) {
@@ -1773,7 +1856,15 @@ __global__ void __launch_bounds__(kThreads2, 2) k2_pass(PassDev ps, const Acc* _
             if (k == 0) m0 = smask[0], m1 = smask[1];
         }
         const int ob = ssteps[k] - op0, oe = ssteps[k + 1] - op0;
-        if constexpr (MODE == 2) {
+        if constexpr (MODE == 2 && sizeof(Acc) == 8) {
+            run_step_terms64<kWarps, false>(sbase, sbops, ob, oe, warp, lane);
+        } else if constexpr (MODE == 4 && sizeof(Acc) == 8) {
+            const bool direct = k + 1 == tile.nsteps;
+            run_step_terms64<kWarps, true>(sbase, sbops, ob, oe, warp, lane,
+                                           direct ? reinterpret_cast<long long*>(dst) + (size_t)slot * slot_elems + s0
+                                                  : nullptr,
+                                           ld, min(S, H - s0));
+        } else if constexpr (MODE == 2) {
             run_step_terms<Acc, kWarps, false, TMAW>(sbase, sbops, ob, oe, warp, lane, nullptr, 0, 0, swsl, m0, m1);
         } else if constexpr (MODE == 6) {
             // u16 pair mode: the root step widens the packed halves to 32 bits
@@ -2215,6 +2306,10 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         Acc* DST = ws + (size_t)((p + 1) & 1) * g.W * g.ld;
         const size_t smem2 = k2_smem_bytes(g.acc_dtype, ps.max_slots, ps.L, ps.max_tile_ops);
         auto k2 = k2_pass<Acc, Out, 0>;
+        if constexpr (sizeof(Acc) == 8) {
+            // int64: level pairs on 64-bit words; non-root bands store from registers
+            if (ps.pairs) k2 = final_pass ? k2_pass<Acc, Out, 2> : k2_pass<Acc, Out, 4>;
+        }
         if constexpr (sizeof(Acc) == 4) {
             // level pairs; non-root bands (MODE 4) store their columns from registers
             if (ps.pairs) k2 = final_pass ? k2_pass<Acc, Out, 2> : k2_pass<Acc, Out, 4>;

@@ -41,4 +41,18 @@ for in_dt, acc in (("i32", "i32"), ("i64", "i64"), ("i32", "i64"), ("f32", "f32"
         torch.cuda.synchronize()
         ms.append(s.elapsed_time(e))
     m = float(np.median(ms))
-    print(f"{n}x{n} x{b} in={in_dt} acc={acc}: {m:.4f} ms  {sums / m / 1e6:.1f} Gsums/s  launches {plan.launches}")
+    # per-launch times (events between launches, fht_execute_profiled)
+    import ctypes
+
+    from paper_2411_07351_b200._lib import check, lib
+    nl = plan.launches
+    ms_arr, kind_arr, b_arr, got = (ctypes.c_float * nl)(), (ctypes.c_int * nl)(), (ctypes.c_double * nl)(), ctypes.c_int()
+    ptrs = (ctypes.c_void_p * 4)(*[out[q].data_ptr() for q in fht.QUADRANTS])
+    ws = plan.workspace()
+    check(lib().fht_execute_profiled(plan._h, ctypes.c_void_p(x.data_ptr()), n * n, ptrs, n * n,
+                                     ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
+                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ms_arr, kind_arr, b_arr,
+                                     nl, ctypes.byref(got)))
+    names = {1: "K1", 5: "stage", 4: "K1P", 2: "K2", 3: "K2root"}
+    per = " ".join(f"{names[kind_arr[i]]}={ms_arr[i]:.3f}" for i in range(got.value))
+    print(f"{n}x{n} x{b} in={in_dt} acc={acc}: {m:.4f} ms  {sums / m / 1e6:.1f} Gsums/s  [{per}]")
