@@ -2077,16 +2077,19 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
         issue_windows<Acc, kNT>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
         cp_async_commit();
     }
+    const int probe = ps.probe;
     for (int it = 0;; ++it) {
         const int p = it & 1;
-        if constexpr (TMA) {
-            mbar_wait(bars + 8u * p, (it >> 1) & 1);  // this slot's windows (bulk bytes + 4-byte copies)
-        } else {
-            cp_async_wait0();  // this slot's windows
+        if (it == 0 || !(probe & 4)) {
+            if constexpr (TMA) {
+                mbar_wait(bars + 8u * p, (it >> 1) & 1);  // this slot's windows (bulk bytes + 4-byte copies)
+            } else {
+                cp_async_wait0();  // this slot's windows
+            }
         }
         __syncthreads();   // ... visible to all; the last slot's store is done with the other buffer
         const int next = slot + static_cast<int>(gridDim.z);
-        if (next < nslots) {
+        if (next < nslots && !(probe & 4)) {
             if constexpr (TMA) {
                 // the other buffer was last read (and some of its slots
                 // written) through the generic proxy before the barrier above
@@ -2100,7 +2103,7 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
             }
         }
         const int4* ops = sbops + (p ? 2 * nops : 0);
-        for (int k = 0; k < tile.nsteps; ++k) {
+        for (int k = 0; k < ((probe & 1) ? 0 : tile.nsteps); ++k) {
             if (k) __syncthreads();
             if (k + 1 < tile.nsteps) {
                 run_step_terms<Acc, kWarps, false>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
@@ -2114,7 +2117,8 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
         Out* __restrict__ o =
             reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
         const int xs = p ? xs1 : xs0;
-        if constexpr (WIDE) {
+        if (probe & 2) {
+        } else if constexpr (WIDE) {
             store_root_rows<Acc, Out, kWarps>(o, W, t0, nc, sbase + static_cast<uint32_t>(xs & 0xffff) * L * 4u, 0u, s0,
                                               rows, warp, lane);
             if (rows_hi > 0)
@@ -2209,6 +2213,15 @@ int slots_per_cta(int ctas_at_one, int nslots) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 4)}));
+}
+
+// FHT_K2_PROBE (debug timing only, see PassDev::probe)
+int k2_probe() {
+    static const int v = [] {
+        const char* e = std::getenv("FHT_K2_PROBE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
 }
 
 template <class In, class Acc, class Out>
@@ -2320,6 +2333,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         }
         PassDev pd = ps;
         pd.bulk = g.k2_bulk;
+        pd.probe = k2_probe();
         if constexpr (std::is_same<Acc, int32_t>::value) {
             // pair-mode root band with double-buffered windows
             int max_nc = 0;

@@ -83,6 +83,10 @@ struct PassDev {
     int ktma;
     const int* kwslots;
     const int2* kwstores;
+    // timing probe (FHT_K2_PROBE, debug only; results are wrong when set):
+    // bit 0 skips the merges, bit 1 the root store, bit 2 the window copies
+    // after the first slot (k2_pair_pipe)
+    int probe;
 };
 
 struct GroupLaunch {
