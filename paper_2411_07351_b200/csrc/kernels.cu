@@ -2016,7 +2016,8 @@ __device__ __forceinline__ void issue_windows_tma(uint32_t srec, int nwin, const
 // WIDE: tiles of 17..32 slopes on 1024 threads, one CTA per SM (the two
 // window buffers of a 32-slope tile take ~175 KB): half the root store's
 // partial-line writes and fewer windows per slope than 16-slope tiles.
-template <class Out, bool TMA, bool WIDE = false>
+// PROBE: compiled with the FHT_K2_PROBE timing switches (PassDev::probe)
+template <class Out, bool TMA, bool WIDE = false, bool PROBE = false>
 __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
     k2_pair_pipe(PassDev ps, const int* __restrict__ src, long long slot_elems, int W, int H, int ld, OutDesc out,
                  QuadSet qs, int img0, int pmD, int nslots) {
@@ -2077,7 +2078,7 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
         issue_windows<Acc, kNT>(ps, tile, src + (size_t)slot * slot_elems, sbase, L, S, s0, H, ld, warp, lane, 0u, srec);
         cp_async_commit();
     }
-    const int probe = ps.probe;
+    const int probe = PROBE ? ps.probe : 0;
     for (int it = 0;; ++it) {
         const int p = it & 1;
         if (it == 0 || !(probe & 4)) {
@@ -2346,7 +2347,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                                    static_cast<size_t>(ps.pipe_loads) * sizeof(int4) * (tma ? 2 : 1) +  // window records
                                    16;                                                                   // mbarriers
                 auto kp = wide ? (tma ? k2_pair_pipe<Out, true, true> : k2_pair_pipe<Out, false, true>)
-                               : (tma ? k2_pair_pipe<Out, true> : k2_pair_pipe<Out, false>);
+                          : pd.probe ? (tma ? k2_pair_pipe<Out, true, false, true> : k2_pair_pipe<Out, false, false, true>)
+                                     : (tma ? k2_pair_pipe<Out, true> : k2_pair_pipe<Out, false>);
                 allow_smem(reinterpret_cast<const void*>(kp));
                 const int rt = (g.pm_D + ps.S - 1) / ps.S;
                 const int spc = slots_per_cta(rt * ps.ntiles * nslots, nslots);
