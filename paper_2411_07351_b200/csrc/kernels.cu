@@ -1496,7 +1496,7 @@ __global__ void __launch_bounds__(kThreadsBYP, 2) k1_by32_pair(QuadSet qs, int W
                                                                 const int* __restrict__ bx0, Acc* __restrict__ ws,
                                                                 int nbuf, const unsigned char* __restrict__ stage,
                                                                 long long spitch, long long simg, long long st_t,
-                                                                long long st_p, int pmD) {
+                                                                long long st_p, int pmD, int ahead) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* sm = reinterpret_cast<Acc*>(smem_raw);
@@ -1507,6 +1507,24 @@ __global__ void __launch_bounds__(kThreadsBYP, 2) k1_by32_pair(QuadSet qs, int W
     split_slot(slot, qs.n, img_l, qi);
     const int q = quad_code(qs, qi);
     const unsigned char* __restrict__ sb = stage + (size_t)img_l * simg + (q < 2 ? st_t : st_p);
+    // The staged leaf columns of the block `ahead` CTAs later in launch order
+    // (about one wave: the CTA that will take this SM slot next) are pulled
+    // into L2 by one TMA prefetch, so that CTA's leaf loads hit L2 instead of
+    // waiting on DRAM (the loads are K1P's largest stall).
+    if (ahead > 0 && tid == 0) {
+        const long long lin = blockIdx.y + (long long)gridDim.y * blockIdx.z + ahead;
+        if (lin < (long long)gridDim.y * gridDim.z) {
+            const int y2 = static_cast<int>(lin % gridDim.y), z2 = static_cast<int>(lin / gridDim.y);
+            int img2, qi2;
+            split_slot(z2, qs.n, img2, qi2);
+            const int q2 = quad_code(qs, qi2);
+            const int c0 = bx0[y2];
+            const int cf = (q2 & 1) ? W - kBYW - c0 : c0;  // the first column in memory (reversed sets)
+            const unsigned char* p2 = stage + (size_t)img2 * simg + (q2 < 2 ? st_t : st_p) + (size_t)cf * spitch;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p2),
+                         "r"(static_cast<uint32_t>(kBYW * spitch)) : "memory");
+        }
+    }
     by_level12_staged_pair<Acc, kThreadsBYP / 8>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0, pmD);
     __syncthreads();
     if (warp < kWarpsBY) {
@@ -2216,6 +2234,16 @@ int slots_per_cta(int ctas_at_one, int nslots) {
     return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 4)}));
 }
 
+// K1P's L2 prefetch distance in CTAs (launch order): about one wave of two
+// CTAs per SM; FHT_K1P_PREFETCH overrides it (0: off)
+int k1p_prefetch_ahead() {
+    if (const char* e = std::getenv("FHT_K1P_PREFETCH")) return std::max(0, std::atoi(e));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 2 * sms;
+}
+
 // FHT_K2_PROBE (debug timing only, see PassDev::probe)
 int k2_probe() {
     static const int v = [] {
@@ -2291,7 +2319,8 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
                     auto kq = k1_by32_pair<Acc>;
                     allow_smem(reinterpret_cast<const void*>(kq));
                     launch_k(g.pdl, kq, dim3(1, g.nby, nslots), dim3(kThreadsBYP), sm_by, st, g.qs, g.W, g.H, g.ld, g.S,
-                             g.by_x0, ws, g.nbuf, stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D);
+                             g.by_x0, ws, g.nbuf, stage, g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D,
+                             k1p_prefetch_ahead());
                     launched = true;
                 }
             }
