@@ -550,6 +550,50 @@ __device__ __forceinline__ void run_step_widen(uint32_t base, const int4* __rest
     }
 }
 
+// The level-pair step and root step of the pair-mode root band (k2_pair_pipe)
+// with the op records addressed as shared-window offsets: the records are
+// read with ld.shared at a 32-bit address, so no op re-derives the shared
+// window base from a generic pointer (10 uniform instructions per op).
+template <int NWARPS>
+__device__ __forceinline__ void run_step_terms_s(uint32_t base, uint32_t ops, int o_beg, int o_end, int warp, int lane) {
+    using Acc = int;
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 h = lds4u(ops + 32u * o), q = lds4u(ops + 32u * o + 16u);
+        const uint32_t d = base + static_cast<uint32_t>(h.x);
+        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        const int n = h.y, nt = h.z & 7;
+        if (nt == 4) {
+            if (n >= 256 && n < 288) rows_op_terms_256<Acc, 4, 2>(d, t, n, lane);
+            else rows_op_terms<Acc, 4, 2>(d, t, n, lane);
+        } else if (nt == 2) {
+            if (n >= 256 && n < 288) rows_op_terms_256<Acc, 2, 1>(d, t, n, lane);
+            else rows_op_terms<Acc, 2, 1>(d, t, n, lane);
+        } else if (nt == 3) {
+            if ((q.w & 15) == 2) rows_op_terms<Acc, 3, 2>(d, t, n, lane);
+            else rows_op_terms<Acc, 3, 1>(d, t, n, lane);
+        } else {
+            for (int i = lane; i < n; i += 32) sts1u(d + 4u * i, lds1u(t[0] + 4u * i));
+        }
+    }
+}
+template <int NWARPS>
+__device__ __forceinline__ void run_step_widen_s(uint32_t base, uint32_t ops, int o_beg, int o_end, int warp, int lane) {
+    for (int o = o_beg + warp; o < o_end; o += NWARPS) {
+        const int4 h = lds4u(ops + 32u * o), q = lds4u(ops + 32u * o + 16u);
+        const uint32_t d = base + static_cast<uint32_t>(h.x), dh = base + (static_cast<uint32_t>(q.w) >> 4);
+        const uint32_t t[4] = {base + static_cast<uint32_t>(h.w), base + static_cast<uint32_t>(q.x),
+                               base + static_cast<uint32_t>(q.y), base + static_cast<uint32_t>(q.z)};
+        const int n = h.y, nt = h.z & 7, split = q.w & 15;
+        if (nt == 4 && n == 256) rows_op_widen_256<4, 2>(d, dh, t, lane);
+        else if (nt == 4) rows_op_widen<4, 2>(d, dh, t, n, lane);
+        else if (nt == 2) rows_op_widen<2, 1>(d, dh, t, n, lane);
+        else if (nt == 3 && split == 2) rows_op_widen<3, 2>(d, dh, t, n, lane);
+        else if (nt == 3) rows_op_widen<3, 1>(d, dh, t, n, lane);
+        else rows_op_widen<1, 1>(d, dh, t, n, lane);
+    }
+}
+
 template <class Acc, int NWARPS, bool DIRECT, bool WADJ = false>
 __device__ __forceinline__ void run_step_terms(uint32_t base, const int4* __restrict__ ops, int o_beg, int o_end,
                                                int warp, int lane, Acc* __restrict__ gdst = nullptr, int ld = 0,
@@ -2057,6 +2101,7 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
     int* ssteps = reinterpret_cast<int*>(sbops + 4 * ps.max_tile_ops);
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid] - op0;
+    const uint32_t sops0 = smem_u32(sbops);
     {
         const int4* __restrict__ b0 = TMA ? ps.tbops : ps.bops;
         const int4* __restrict__ b1 = TMA ? ps.tbops1 : ps.bops1;
@@ -2121,13 +2166,13 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
                 cp_async_commit();
             }
         }
-        const int4* ops = sbops + (p ? 2 * nops : 0);
+        const uint32_t ops = sops0 + (p ? 32u * static_cast<uint32_t>(nops) : 0u);
         for (int k = 0; k < ((probe & 1) ? 0 : tile.nsteps); ++k) {
             if (k) __syncthreads();
             if (k + 1 < tile.nsteps) {
-                run_step_terms<Acc, kWarps, false>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+                run_step_terms_s<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
             } else {
-                run_step_widen<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+                run_step_widen_s<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
             }
         }
         __syncthreads();
