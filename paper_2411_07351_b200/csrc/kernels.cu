@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, const int4* __restrict__ bops, int max_width,
     int sr, int max_ops,
     Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
-    long long spitch, long long simg, long long st_t, long long st_p, int pmD) {
+    long long spitch, long long simg, long long st_t, long long st_p, int pmD, int k1_ahead) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Acc* buf0 = reinterpret_cast<Acc*>(smem_raw);  // slots [0, max_width): parity 0
@@ -803,6 +803,24 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const int q = quad_code(qs, qi);
     const In* __restrict__ im = img + (size_t)img_i * img_stride;
     const int s0 = blockIdx.x * S;
+    // staged pair mode: pull the leaf columns of the block `k1_ahead` CTAs
+    // later in launch order into L2 (as K1P does)
+    if (stage != nullptr && pmD && k1_ahead > 0 && tid == 0) {
+        const long long gx = gridDim.x, gy = gridDim.y;
+        const long long lin = blockIdx.x + gx * (blockIdx.y + gy * (long long)blockIdx.z) + k1_ahead;
+        if (lin < gx * gy * gridDim.z) {
+            const int y2 = static_cast<int>((lin / gx) % gy), z2 = static_cast<int>(lin / (gx * gy));
+            int il2, qi2;
+            split_slot(z2, nq, il2, qi2);
+            const int q2 = quad_code(qs, qi2);
+            const int4 b2 = blocks[y2];
+            const int w2 = shapes[b2.y].width;
+            const int cf = (q2 & 1) ? W - w2 - b2.x : b2.x;
+            const unsigned char* p2 = stage + (size_t)il2 * simg + (q2 < 2 ? st_t : st_p) + (size_t)cf * spitch;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p2), "r"(static_cast<uint32_t>(w2 * spitch))
+                         : "memory");
+        }
+    }
 
     // Load the tile: values of depth `nsteps` (the leaves) into buf[nsteps & 1].
     Acc* lbuf = (nsteps & 1) ? buf1 : buf0;
@@ -2279,6 +2297,12 @@ int slots_per_cta(int ctas_at_one, int nslots) {
     return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 4)}));
 }
 
+// K1's (pair mode) L2 prefetch distance; FHT_K1_PREFETCH (0: off)
+int k1_prefetch_ahead() {
+    if (const char* e = std::getenv("FHT_K1_PREFETCH")) return std::max(0, std::atoi(e));
+    return 64;
+}
+
 // K1P's L2 prefetch distance in CTAs (launch order): about one wave of two
 // CTAs per SM; FHT_K1P_PREFETCH overrides it (0: off)
 int k1p_prefetch_ahead() {
@@ -2344,7 +2368,7 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         launch_k(g.pdl && !both, k1, g1, dim3(kThreads), smem, st1, reinterpret_cast<const In*>(g.img), g.img_w,
                  g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes, g.step_offs,
                  g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf, g.root_is_block, g.out, stage,
-                 g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D);
+                 g.stage_pitch, g.stage_img, g.stage_t, g.stage_p, g.pm_D, k1_prefetch_ahead());
         ++launches;
         if (hook) hook(ctx, 1);
     }
