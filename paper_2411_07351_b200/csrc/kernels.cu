@@ -2288,13 +2288,14 @@ void allow_smem(const void* fn) {
 }
 
 // Slots one k2_pair_pipe CTA walks: FHT_K2_SLOTS_PER_CTA, else as many as
-// keep >= 4 waves of 2 CTAs per SM, at most 8 (measured best for c4).
+// keep >= 3 waves of 2 CTAs per SM, at most 8 (measured best for c4: 8 at
+// 256 images, 4 at the 32 images of a rank under 8-GPU strong scaling).
 int slots_per_cta(int ctas_at_one, int nslots) {
     if (const char* e = std::getenv("FHT_K2_SLOTS_PER_CTA")) return std::max(1, std::min(64, std::atoi(e)));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 4)}));
+    return std::max(1, std::min({8, nslots, ctas_at_one / (sms * 2 * 3)}));
 }
 
 // K1's (pair mode) L2 prefetch distance; FHT_K1_PREFETCH (0: off)
