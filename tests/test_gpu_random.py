@@ -47,3 +47,21 @@ def test_random_plans(seed):
                 got = out[q][bi].cpu().numpy()
                 exp = ref[q] if layout == "reference" else ref[q].T
                 assert np.array_equal(got, exp.astype(got.dtype)), (h, w, strategy, kind, layout, q, bi)
+
+
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_every_narrow_width(strategy):
+    """Every width 1..70 (all remainder-block shapes below and around one
+    32-block, the K1 / K1P split, the first bands) at a few heights, all four
+    quadrants, u8 -> i32, bit-exact against the oracle."""
+    rng = np.random.default_rng(77 + strategy)
+    for w in range(1, 71):
+        for h in (1, 6, 37):
+            imgs = rng.integers(0, 256, (2, h, w)).astype(np.uint8)
+            plan = fht.Plan(w, h, strategy, in_dtype="u8", acc_dtype="i32", batch=2)
+            out = plan(torch.from_numpy(imgs).cuda())
+            torch.cuda.synchronize()
+            for b in range(2):
+                ref, _ = oracle.fht2d_quadrants(imgs[b], strategy, dtype=np.int32)
+                for k in Q:
+                    np.testing.assert_array_equal(out[k][b].cpu().numpy(), ref[k], err_msg=f"{h}x{w} {k} s{strategy}")

@@ -153,3 +153,34 @@ def test_batch_baseline_helpers_agree():
     np.testing.assert_array_equal(a, b)
     q, _ = oracle.ref_fht2d_quadrants(imgs[1].astype(np.int64), T)
     np.testing.assert_array_equal(a[1, 2], q["vert_pos"].ravel())
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_port_matches_compiled_reference_every_small_shape():
+    """Every w, h <= 20, both strategies, all four quadrants and the addition
+    counts, against the reference library compiled from its own sources
+    (transform.cpp:62-85, quadrants.cpp:23-41)."""
+    rng = np.random.default_rng(5)
+    for h in range(1, 21):
+        for w in range(1, 21):
+            img = rng.integers(-1000, 1000, (h, w))
+            for strat in (S, T):
+                qr, tr = oracle.ref_fht2d_quadrants(img, strat)
+                qp, tp = oracle.fht2d_quadrants(img, strat)
+                assert tr == tp, (h, w, strat)
+                for k in oracle.QUADRANTS:
+                    np.testing.assert_array_equal(qr[k], qp[k], err_msg=f"{h}x{w} {k} strategy {strat}")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_port_matches_compiled_reference_random_shapes():
+    """Seeded random shapes up to 300 wide (non-powers of two, thin images)."""
+    rng = np.random.default_rng(6)
+    for _ in range(12):
+        h, w = (int(v) for v in rng.integers(1, 301, 2))
+        strat = int(rng.integers(0, 2))
+        img = rng.integers(0, 256, (h, w))
+        jr, ar = oracle.ref_fht2d_counted(img, strat)
+        jp, ap = oracle.fht2d_counted_i64(img, strat)
+        np.testing.assert_array_equal(jr, jp, err_msg=f"{h}x{w} strategy {strat}")
+        assert ar == ap
