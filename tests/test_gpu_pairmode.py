@@ -209,3 +209,27 @@ def test_wide_root_band_tiles(monkeypatch, h, w, strategy):
             ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
             for k in Q:
                 np.testing.assert_array_equal(out[k][bi], ref[k], err_msg=f"{h}x{w} tma{tma} {k} img{bi}")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pair_mode_random_shapes(seed):
+    """Seeded random pair-mode shapes (65..512 wide, 64..512 high), both
+    strategies, random batches and quadrant masks, some all-255 images (the
+    16-bit limit): bit-exact against the oracle (scripts/pair_sweep.py runs
+    the same sweep at length)."""
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(15):
+        w, h = int(rng.integers(65, 513)), int(rng.integers(64, 513))
+        strategy, b, mask = int(rng.integers(2)), int(rng.integers(1, 4)), int(rng.integers(1, 16))
+        quads = [q for i, q in enumerate(oracle.QUADRANTS) if mask & (1 << i)]
+        imgs = rng.integers(0, 256, (b, h, w)).astype(np.uint8)
+        if rng.random() < 0.2:
+            imgs[:] = 255
+        plan = fht.Plan(w, h, strategy, in_dtype="u8", acc_dtype="i32", quadrants=quads, batch=b)
+        assert any(g["u16_pair_D"] for g in plan.describe()["groups"])
+        out = plan(torch.from_numpy(imgs).cuda())
+        torch.cuda.synchronize()
+        for bi in range(b):
+            ref, _ = oracle.fht2d_quadrants(imgs[bi], strategy, dtype=np.int32)
+            for k in quads:
+                np.testing.assert_array_equal(out[k][bi].cpu().numpy(), ref[k], err_msg=f"{h}x{w} s{strategy} {k}")
