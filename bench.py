@@ -475,6 +475,10 @@ def run_ours(args):
             tr = pj.get(args.config, {}).get(names[dom])
             if tr:
                 roofline["traffic"] = tr
+                # ncu cannot run inside the timed bench: the DRAM bytes (and the
+                # LSU / issue fractions below) come from one --set full capture of
+                # this build, regenerated with every kernel change
+                roofline["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full, same build)"
             # what actually binds the kernel (ncu, same capture): LSU/shared
             # data-pipe wavefronts and issue slots, as fractions of peak
             lsu = pj.get("lsu_issue", {}).get(args.config, {}).get(names[dom])
