@@ -2119,6 +2119,8 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
     int* ssteps = reinterpret_cast<int*>(sbops + 4 * ps.max_tile_ops);
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid] - op0;
+    const int so1 = tile.nsteps >= 1 ? ps.step_offs[tile.step_beg + 1] - op0 : 0;
+    const int so2 = tile.nsteps >= 2 ? ps.step_offs[tile.step_beg + 2] - op0 : 0;
     const uint32_t sops0 = smem_u32(sbops);
     {
         const int4* __restrict__ b0 = TMA ? ps.tbops : ps.bops;
@@ -2185,12 +2187,16 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
             }
         }
         const uint32_t ops = sops0 + (p ? 32u * static_cast<uint32_t>(nops) : 0u);
+        // the op ranges of the first two steps (all of a root band of <= 4
+        // levels) come from registers, not from the shared step table
         for (int k = 0; k < ((probe & 1) ? 0 : tile.nsteps); ++k) {
             if (k) __syncthreads();
+            const int lo = k == 0 ? 0 : k == 1 ? so1 : ssteps[k];
+            const int hi = k == 0 ? so1 : k == 1 ? so2 : ssteps[k + 1];
             if (k + 1 < tile.nsteps) {
-                run_step_terms_s<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+                run_step_terms_s<kWarps>(sbase, ops, lo, hi, warp, lane);
             } else {
-                run_step_widen_s<kWarps>(sbase, ops, ssteps[k], ssteps[k + 1], warp, lane);
+                run_step_widen_s<kWarps>(sbase, ops, lo, hi, warp, lane);
             }
         }
         __syncthreads();
