@@ -2119,6 +2119,13 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
     const int op0 = ps.step_offs[tile.step_beg], nops = ps.step_offs[tile.step_beg + tile.nsteps] - op0;
     int* ssteps = reinterpret_cast<int*>(sbops + 4 * ps.max_tile_ops);
     if (tid <= tile.nsteps) ssteps[tid] = ps.step_offs[tile.step_beg + tid] - op0;
+    const bool oq_fixed = static_cast<int>(gridDim.z) % qs.n == 0;
+    Out* __restrict__ oq = nullptr;  // (oq_fixed) the CTA's quadrant output, at image img0
+    if (oq_fixed) {
+        int img_l, qi;
+        split_slot(slot, qs.n, img_l, qi);
+        oq = reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)img0 * out.img_stride;
+    }
     const int so1 = tile.nsteps >= 1 ? ps.step_offs[tile.step_beg + 1] - op0 : 0;
     const int so2 = tile.nsteps >= 2 ? ps.step_offs[tile.step_beg + 2] - op0 : 0;
     const uint32_t sops0 = smem_u32(sbops);
@@ -2200,10 +2207,18 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
             }
         }
         __syncthreads();
-        int img_l, qi;
-        split_slot(slot, qs.n, img_l, qi);
-        Out* __restrict__ o =
-            reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
+        // this slot's output image: the quadrant is the same for every slot of
+        // the CTA when the slot stride is a multiple of the quadrant count
+        Out* __restrict__ o;
+        if (oq_fixed) {
+            int img_l, qi;
+            split_slot(slot, qs.n, img_l, qi);
+            o = oq + (size_t)img_l * out.img_stride;
+        } else {
+            int img_l, qi;
+            split_slot(slot, qs.n, img_l, qi);
+            o = reinterpret_cast<Out*>(out_ptr(out, quad_code(qs, qi))) + (size_t)(img0 + img_l) * out.img_stride;
+        }
         const int xs = p ? xs1 : xs0;
         if (probe & 2) {
         } else if constexpr (WIDE) {
