@@ -2086,6 +2086,25 @@ __device__ __forceinline__ void issue_windows_tma(uint32_t srec, int nwin, const
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// issue_windows_tma on the warps [w0, nw) only (window w -> warp w0 + w mod
+// (nw - w0)); no arrival -- every thread arrives separately (tma_arrive).
+__device__ __forceinline__ void issue_windows_tma_on(uint32_t srec, int nwin, const int* __restrict__ in, int ld,
+                                                     uint32_t stage, int H, int warp, int lane, uint32_t bar, int w0,
+                                                     int nw) {
+    if (warp < w0) return;
+    for (int w = warp - w0; w < nwin; w += nw - w0) {
+        const int4 r0 = lds4u(srec + 32u * w), r1 = lds4u(srec + 32u * w + 16u);
+        const int* __restrict__ col = in + (size_t)r0.x * ld;
+        if (lane == 0 && r0.w > 0) bulk_copy(stage + static_cast<uint32_t>(r0.y), col + r0.z, 4u * r0.w, bar);
+        uint32_t d = stage + static_cast<uint32_t>(r1.x) + 4u * lane;
+        int sw = r1.y + lane;
+        for (int i = lane; i < r1.z; i += 32, d += 128u, sw += 32) cp_async4(d, col + (sw >= H ? sw - H : sw));
+    }
+}
+__device__ __forceinline__ void tma_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+
 // ------------------------------------------------------- K2, pair mode
 // The u16 pair mode root band with double-buffered windows: each CTA keeps
 // its tile and walks slots (grid.z strided).  While slot i computes, the
@@ -2180,7 +2199,11 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
         }
         __syncthreads();   // ... visible to all; the last slot's store is done with the other buffer
         const int next = slot + static_cast<int>(gridDim.z);
-        if (next < nslots && !(probe & 4)) {
+        // (TMA, two steps: the next slot's windows are issued after step 0,
+        // by the warps that have one op fewer in it -- they would wait at the
+        // step barrier anyway -- so no warp starts its first op late)
+        const bool defer = TMA && !WIDE && tile.nsteps == 2;
+        if (next < nslots && !(probe & 4) && !defer) {
             if constexpr (TMA) {
                 // the other buffer was last read (and some of its slots
                 // written) through the generic proxy before the barrier above
@@ -2197,7 +2220,19 @@ __global__ void __launch_bounds__(WIDE ? 1024 : kThreads2, WIDE ? 1 : 2)
         // the op ranges of the first two steps (all of a root band of <= 4
         // levels) come from registers, not from the shared step table
         for (int k = 0; k < ((probe & 1) ? 0 : tile.nsteps); ++k) {
-            if (k) __syncthreads();
+            if (k) {
+                if constexpr (TMA && !WIDE) {
+                    if (defer && k == 1 && next < nslots && !(probe & 4)) {
+                        // warps [so1 - kWarps, kWarps) ran one op fewer in step 0 (all warps when so1 <= kWarps)
+                        const int w0 = so1 > kWarps ? min(so1 - kWarps, kWarps - 1) : 0;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_windows_tma_on(srec, tile.load_cnt, src + (size_t)next * slot_elems, ld,
+                                             sbase + (p ? 0u : alt), H, warp, lane, bars + 8u * (1 - p), w0, kWarps);
+                        tma_arrive(bars + 8u * (1 - p));
+                    }
+                }
+                __syncthreads();
+            }
             const int lo = k == 0 ? 0 : k == 1 ? so1 : ssteps[k];
             const int hi = k == 0 ? so1 : k == 1 ? so2 : ssteps[k + 1];
             if (k + 1 < tile.nsteps) {
