@@ -45,6 +45,13 @@ enum { FHT_SPLIT_SIMPLE = 0, FHT_SPLIT_TWEAKED = 1 };
 /* Element types. */
 enum { FHT_U8 = 0, FHT_I32 = 1, FHT_I64 = 2, FHT_F32 = 3 };
 
+/* Accumulator code for fht_plan_create: int64 accumulation whose pass 0
+ * (the width-<=32 blocks) may accumulate in int32 because the caller knows
+ * 32 * max|value| < 2^31 (inputs i32 / i64).  Results are identical to
+ * FHT_I64; the reference-style int64 entry points choose it themselves after
+ * their overflow check (transform.cpp:16-27). */
+enum { FHT_I64_PASS0_I32 = FHT_I64 | 0x100 };
+
 /* Quadrant bits, QuadrantSet order (quadrants.hpp:15-28). */
 enum {
     FHT_HORIZ_POS = 1, /* fht2d(I)                       */

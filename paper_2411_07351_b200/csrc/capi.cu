@@ -127,6 +127,7 @@ struct Group {
     long long stage_img = 0, stage_pitch = 0, stage_t = -1, stage_p = -1;
     std::vector<int> pass_S, pass_L;  // K2 rows per tile and slot capacity, per pass
     int pm_D = 0;  // u16 pair mode (0: off): workspace words pair rows j and j + pm_D
+    bool k1_acc32 = false;  // int64 plan, pass 0 in int32 (GroupLaunch::k1_acc32)
     size_t slot_bytes = 0;
     size_t acc_sz = 4;  // accumulator bytes
 };
@@ -639,8 +640,10 @@ int pass_rows(const fhtb::FusedPass& ps, int max_slots, int H, size_t esz, size_
 
 int block_width_default() { return env_int("FHT_BLOCK_WIDTH", 32, 1, 64); }
 
+// k1_acc32: an int64 plan whose pass 0 may accumulate in int32 (the caller
+// knows 32 * max|v| < 2^31; the int64 reference entry points, run_i64)
 fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, int mask, int batch, int layout,
-                        int device) {
+                        int device, bool k1_acc32 = false) {
     if (w < 1 || h < 1) throw std::invalid_argument("fht2d: image is empty");
     if (strategy != FHT_SPLIT_SIMPLE && strategy != FHT_SPLIT_TWEAKED)
         throw std::invalid_argument("unknown strategy (expected simple|tweaked)");
@@ -735,6 +738,10 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             tw = std::max(1, tw / 2);
         }
         g->pm_D = pm ? pmD : 0;
+        // int64 accumulation with pass 0 in int32: blocks of width <= 32
+        // (Simple trees with a wider root block keep int64 pass 0)
+        g->k1_acc32 = k1_acc32 && acc_sz == 8 && in != FHT_U8 && in != FHT_F32 && bw <= 32 &&
+                      env_int("FHT_K1_ACC32", 1, 0, 1) == 1;
         g->acc_sz = acc_sz;
         g->qs.n = static_cast<int>(codes.size());
         for (int k = 0; k < 4; ++k) g->qs.code[k] = k < g->qs.n ? codes[static_cast<size_t>(k)] : 0;
@@ -742,7 +749,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         // K1 rows per tile: every op's window (S + halo) fits the executor's
         // 256-row item pair.
         // K1 rows per tile: the fewest tiles of <= 256 rows, balanced.
-        const int smax = acc_sz == 8 ? 128 : env_int("FHT_K1_SMAX", 256, 16, 256);
+        const int smax = acc_sz == 8 && !g->k1_acc32 ? 128 : env_int("FHT_K1_SMAX", 256, 16, 256);
         const int ntile = (H + smax - 1) / smax;
         int S = ((H + ntile - 1) / ntile + 7) & ~7;
         if (H < S) S = H;
@@ -758,7 +765,7 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
             g->sr = sr;
         }
         g->nbuf = g->sp.root_is_block ? 0 : (g->sp.passes.size() > 1 ? 2 : 1);
-        g->use_by32 = acc_sz == 4 && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
+        g->use_by32 = (acc_sz == 4 || g->k1_acc32) && env_int("FHT_K1_BY32", 1, 0, 1) == 1;
         // staging pays off once the batch is large (its launch costs a few
         // microseconds: a loss for one small image); FHT_K1_STAGE=0/1 forces it
         const int stage_env = env_int("FHT_K1_STAGE", -1, -1, 1);
@@ -807,7 +814,8 @@ fht_plan_s* create_plan(int w, int h, int strategy, int in, int acc, int out, in
         bool fits = g->nby <= 65535 && g->nblocks <= 65535;
         for (const auto& d : g->dt.passes) fits = fits && d.ntiles <= 65535;
         if (!fits) throw std::invalid_argument("fht2d: working width too large (more than 65535 tiles per pass)");
-        const size_t smem = fhtb::k1_smem_bytes(acc, g->sp.max_block_width, g->sr, g->dt.max_ops, g->dt.max_steps);
+        const size_t smem = fhtb::k1_smem_bytes(g->k1_acc32 ? FHT_I32 : acc, g->sp.max_block_width, g->sr, g->dt.max_ops,
+                                                g->dt.max_steps);
         if (smem > 227 * 1024) throw FhtError(FHT_ERR_INTERNAL, "K1 tile exceeds shared memory");
         max_slot_bytes = std::max(max_slot_bytes, g->slot_bytes * g->qs.n);
         if (g->nby > 0 || g->pm_D) p->stage_bytes_img = std::max(p->stage_bytes_img, static_cast<size_t>(g->stage_img));
@@ -879,6 +887,7 @@ void execute(fht_plan_s* p, const void* d_in, int64_t in_stride, void* const d_o
             L.nby = g.nby;
             L.by_x0 = g.dt.by_x0;
             L.k1p_variant = g.pm_D ? 5 : env_int("FHT_K1P_VARIANT", 5, 0, 5);  // see GroupLaunch
+            L.k1_acc32 = g.k1_acc32 ? 1 : 0;
             L.pm_D = g.pm_D;
             L.k1p_pair576 = env_int("FHT_K1P_PAIR576", 1, 0, 1);
             L.k1p_576 = env_int("FHT_K1P_576", 1, 0, 1);
@@ -983,7 +992,8 @@ void execute_host(fht_plan_s* p, const void* h_in, void* const h_out[4], cudaStr
 }
 
 // absmax on device -> (ok_for_i32, within 2^62 budget)
-void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok_i32, cudaStream_t st) {
+void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok_i32, cudaStream_t st,
+                  unsigned long long* vmax_out = nullptr) {
     if (dtype == FHT_U8) {
         if (ok_i32) *ok_i32 = static_cast<int64_t>(width) * 255 < (int64_t(1) << 31);
         return;
@@ -1000,6 +1010,7 @@ void check_budget(const void* d_in, int dtype, int64_t count, int width, int* ok
     const unsigned __int128 prod = static_cast<unsigned __int128>(static_cast<unsigned>(width)) * vmax;
     if (prod >= (static_cast<unsigned __int128>(1) << 62))
         throw std::overflow_error("fht2d: width * max|value| reaches 2^62; sums could overflow 64-bit accumulators");
+    if (vmax_out) *vmax_out = vmax;
     if (ok_i32) *ok_i32 = prod < (static_cast<unsigned __int128>(1) << 31);
 }
 
@@ -1020,9 +1031,10 @@ PlanCache& plan_cache() {
     return *c;
 }
 
-std::shared_ptr<fht_plan_s> cached_plan(int w, int h, int strategy, int acc, int mask, int device) {
+std::shared_ptr<fht_plan_s> cached_plan(int w, int h, int strategy, int acc, int mask, int device,
+                                        bool k1_acc32 = false) {
     PlanCache& c = plan_cache();
-    const auto key = std::make_tuple(w, h, strategy, acc, mask, device);
+    const auto key = std::make_tuple(w, h, strategy, acc + (k1_acc32 ? 1000 : 0), mask, device);
     {
         std::lock_guard<std::mutex> lk(c.mu);
         for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
@@ -1033,7 +1045,8 @@ std::shared_ptr<fht_plan_s> cached_plan(int w, int h, int strategy, int acc, int
     }
     // build outside the lock (plan creation uploads tables); a racing thread
     // may build the same plan, the first insert wins
-    std::shared_ptr<fht_plan_s> p(create_plan(w, h, strategy, FHT_I64, acc, FHT_I64, mask, 1, FHT_LAYOUT_REFERENCE, device));
+    std::shared_ptr<fht_plan_s> p(
+        create_plan(w, h, strategy, FHT_I64, acc, FHT_I64, mask, 1, FHT_LAYOUT_REFERENCE, device, k1_acc32));
     std::vector<std::shared_ptr<fht_plan_s>> evicted;  // destroyed after the lock is released
     {
         std::lock_guard<std::mutex> lk(c.mu);
@@ -1115,9 +1128,12 @@ void run_i64(const int64_t* img, int w, int h, int strategy, int mask, int64_t* 
         cuda_check(cudaMemcpyAsync(d_in, img, cells * 8, cudaMemcpyHostToDevice, st), "H2D");
         // check_overflow_budget (transform.cpp:16-27) for every quadrant's working width.
         int ok32 = 0;
+        unsigned long long vmax = 0;
         const int wmax = std::max((mask & 3) ? w : 0, (mask & 12) ? h : 0);
-        check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), wmax, &ok32, st);
-        const std::shared_ptr<fht_plan_s> sp = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev);
+        check_budget(d_in, FHT_I64, static_cast<int64_t>(cells), wmax, &ok32, st, &vmax);
+        // int64 sums needed, but width-32 blocks stay inside int32: pass 0 in int32
+        const bool k1_32 = !ok32 && 32ull * vmax < (1ull << 31);
+        const std::shared_ptr<fht_plan_s> sp = cached_plan(w, h, strategy, ok32 ? FHT_I32 : FHT_I64, mask, dev, k1_32);
         fht_plan_s* p = sp.get();
         for (int q = 0; q < 4; ++q)
             if (mask & (1 << q)) cuda_check(counted_malloc_async(&d_out[q], cells * 8, st), "counted_malloc_async(out)");
@@ -1142,8 +1158,10 @@ int fht_plan_create(int width, int height, int strategy, int in_dtype, int acc_d
                     int quadrant_mask, int batch, int layout, int device, fht_plan_t* plan) {
     return guarded([&] {
         if (!plan) throw std::invalid_argument("null plan pointer");
+        const bool p0 = acc_dtype == FHT_I64_PASS0_I32;
+        if (p0) acc_dtype = FHT_I64;
         *plan = create_plan(width, height, strategy, in_dtype, acc_dtype, out_dtype, quadrant_mask, batch, layout,
-                            device);
+                            device, p0);
     });
 }
 

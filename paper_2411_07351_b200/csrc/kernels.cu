@@ -774,14 +774,16 @@ void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sm
 
 // ------------------------------------------------------------------- K1
 // grid: x = row tile (S rows), y = block, z = slot (image * nq + quadrant idx)
-template <class In, class Acc, class Out, bool SC>
+// WsT: the pass-0 buffer's element type (wider than Acc for the int64 plans'
+// pass 0 in int32, GroupLaunch::k1_acc32)
+template <class In, class Acc, class Out, bool SC, class WsT = Acc>
 __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     const In* __restrict__ img, int img_w, int img_h, long long img_pitch, long long img_stride, int img0, QuadSet qs,
     int W, int H,
     int ld, int S, const int4* __restrict__ blocks, const ShapeHdr* __restrict__ shapes,
     const int* __restrict__ step_offs, const PassOpDev* __restrict__ ops, const int4* __restrict__ bops, int max_width,
     int sr, int max_ops,
-    Acc* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
+    WsT* __restrict__ ws, int nbuf, bool root_is_block, OutDesc out, const unsigned char* __restrict__ stage,
     long long spitch, long long simg, long long st_t, long long st_p, int pmD, int k1_ahead) {
     grid_dep_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -905,17 +907,17 @@ __global__ void __launch_bounds__(kThreads, 2) k1_blocks(
     // Store the block root's S rows (values of local depth 0 live in buf0).
     const int rows_out = min(S, H - s0);
     if (!root_is_block) {
-        Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;  // pass 0 output: buffer 0
+        WsT* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;  // pass 0 output: buffer 0
         const bool al = ((ld | s0) & 3) == 0;
         for (int c = warp; c < wb; c += kWarps)
-            warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, buf0 + c * sr, rows_out, al, lane);
+            warp_store_col<Acc, WsT>(dstw + (size_t)(x0 + c) * ld + s0, buf0 + c * sr, rows_out, al, lane);
         if (pmD) {  // u16 pair mode: words [D, H) from words k and k + e of the root
             const int e = 2 * pmD - H;
             for (int c = warp; c < wb; c += kWarps) {
                 const Acc* rc = buf0 + c * sr;
-                Acc* __restrict__ gc = dstw + (size_t)(x0 + c) * ld + pmD;
+                WsT* __restrict__ gc = dstw + (size_t)(x0 + c) * ld + pmD;
                 for (int k = lane; k < H - pmD; k += 32)
-                    gc[k] = from_bits<Acc>(pair_extra_word(to_bits<Acc>(rc[k]), to_bits<Acc>(rc[k + e])));
+                    gc[k] = static_cast<WsT>(from_bits<Acc>(pair_extra_word(to_bits<Acc>(rc[k]), to_bits<Acc>(rc[k + e]))));
             }
         }
     } else {
@@ -1108,15 +1110,17 @@ __device__ __forceinline__ void by_level_s(Acc* sm, int S, int warp, int lane) {
 
 // Levels 3, 4 (shared memory, rows interleaved over lanes) and 5 (stored
 // from registers); full 256-row tiles take the compile-time row count.
-template <class Acc>
-__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+template <class Acc, class WsT = Acc>
+__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, WsT* __restrict__ dcol0, int ld,
                                               int rows_out, bool act = true);
 
 // Level 5 (the block root) written straight to the pass-0 buffer from
 // registers: lane = row, so each warp store is 32 consecutive rows of one
 // column (coalesced), and the root never round-trips through shared memory.
-template <class Acc, int SF = 0>
-__device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+// WsT: the pass-0 buffer's element type (int64 for the int64 plans' pass 0
+// in int32, see GroupLaunch::k1_acc32): the block root widened on the store.
+template <class Acc, int SF = 0, class WsT = Acc>
+__device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int lane, WsT* __restrict__ dcol0, int ld,
                                                 int rows_out_) {
     const int rows_out = SF ? SF : rows_out_;  // SF: a full tile, rows known at compile time
     constexpr int w = 32, w0 = 16;
@@ -1130,7 +1134,7 @@ __device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int la
         const int r = T - t0;
         const uint32_t a = base + (src + t0) * kBYSR * 4u;
         const uint32_t b = base + ((src + w0 + t0) * kBYSR + r) * 4u;
-        Acc* __restrict__ g = dcol0 + (size_t)T * ld + lane;
+        WsT* __restrict__ g = dcol0 + (size_t)T * ld + lane;
         int x[G], y[G];
 #pragma unroll
         for (int u = 0; u < G; ++u)
@@ -1140,12 +1144,12 @@ __device__ __forceinline__ void by_level5_store(Acc* sm, int S, int warp, int la
             }
 #pragma unroll
         for (int u = 0; u < G; ++u)
-            if (32 * u + lane < rows_out) g[32 * u] = from_bits<Acc>(add_bits<Acc>(x[u], y[u]));
+            if (32 * u + lane < rows_out) g[32 * u] = static_cast<WsT>(from_bits<Acc>(add_bits<Acc>(x[u], y[u])));
     }
 }
 
-template <class Acc>
-__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, Acc* __restrict__ dcol0, int ld,
+template <class Acc, class WsT>
+__device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane, WsT* __restrict__ dcol0, int ld,
                                               int rows_out, bool act) {
     if (S == kBYMaxS) {
         if (act) by_level_s<Acc, 3, 0, kBYMaxS>(sm, S, warp, lane);
@@ -1159,9 +1163,9 @@ __device__ __forceinline__ void by_levels_345(Acc* sm, int S, int warp, int lane
     __syncthreads();
     if (!act) return;
     if (rows_out == kBYMaxS)  // a full tile (the last row tile may be shorter)
-        by_level5_store<Acc, kBYMaxS>(sm, S, warp, lane, dcol0, ld, rows_out);
+        by_level5_store<Acc, kBYMaxS, WsT>(sm, S, warp, lane, dcol0, ld, rows_out);
     else
-        by_level5_store<Acc>(sm, S, warp, lane, dcol0, ld, rows_out);
+        by_level5_store<Acc, 0, WsT>(sm, S, warp, lane, dcol0, ld, rows_out);
 }
 
 template <class Acc, int L, int F = 0>
@@ -1358,11 +1362,11 @@ __device__ __forceinline__ void by_level5_store_pair(Acc* sm, int warp, int lane
 }
 
 // grid: x = row tile, y = BY-32 block, z = slot.  Writes pass-0 buffer 0.
-template <class In, class Acc, int V, int NT = kThreadsBY>
+template <class In, class Acc, int V, int NT = kThreadsBY, class WsT = Acc>
 __global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int img_w, int img_h,
                                                           long long img_pitch, long long img_stride, int img0, QuadSet qs, int W, int H,
                                                           int ld, int S, const int* __restrict__ bx0,
-                                                          Acc* __restrict__ ws, int nbuf,
+                                                          WsT* __restrict__ ws, int nbuf,
                                                           const unsigned char* __restrict__ stage, long long spitch,
                                                           long long simg, long long st_t, long long st_p, int pmD) {
     grid_dep_wait();
@@ -1382,6 +1386,7 @@ __global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int
     Acc* leaves = sm + kBYW * kBYSR;  // parity 1
     constexpr int kRowsPerLane = (kBYMaxS + kBYW - 1 + 31) / 32;  // 9
     static_assert(NT == kThreadsBY || (NT == kThreadsBYP && V == 5), "576 threads: variant 5 only");
+    static_assert(std::is_same<WsT, Acc>::value || V == 5, "a widening pass-0 store: variant 5 only");
     const bool act = NT == kThreadsBY || warp < kWarpsBY;  // the warps that own columns
     if (V == 5 && stage != nullptr) {
         // levels 1-2 read the staged columns directly (no leaf tile)
@@ -1400,14 +1405,16 @@ __global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int
                 by_level_s<Acc, 4>(sm, S, warp, lane);
             }
             __syncthreads();
-            Acc* __restrict__ dcol0 = ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld;
-            if (pmD == kBYMaxS) by_level5_store_pair<Acc, kBYMaxS>(sm, warp, lane, dcol0, ld, pmD, H);
-            else by_level5_store_pair<Acc>(sm, warp, lane, dcol0, ld, pmD, H);
+            if constexpr (std::is_same<WsT, Acc>::value) {
+                Acc* __restrict__ dcol0 = ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld;
+                if (pmD == kBYMaxS) by_level5_store_pair<Acc, kBYMaxS>(sm, warp, lane, dcol0, ld, pmD, H);
+                else by_level5_store_pair<Acc>(sm, warp, lane, dcol0, ld, pmD, H);
+            }
             return;
         }
         by_level12_staged<Acc, NT / 8>(sm, S, tid, sb, spitch, W, x0, (q & 1) != 0);
         __syncthreads();
-        by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+        by_levels_345<Acc, WsT>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
                            min(S, H - s0), act);
         return;
     }
@@ -1509,7 +1516,7 @@ __global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int
     if constexpr (V >= 4) {  // (V = 5 without staging lands here)
         by_level12<Acc, NT / 8>(sm, S, tid);  // levels 1-2 in registers -> slots [0, 32)
         __syncthreads();
-        by_levels_345<Acc>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
+        by_levels_345<Acc, WsT>(sm, S, warp, lane, ws + (size_t)slot * nbuf * W * ld + (size_t)x0 * ld + s0, ld,
                            min(S, H - s0), act);
         return;
     } else if constexpr (V == 3) {
@@ -1541,13 +1548,13 @@ __global__ void __launch_bounds__(NT, 2) k1_by32(const In* __restrict__ img, int
     }
     __syncthreads();
     const int rows_out = min(S, H - s0);
-    Acc* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
+    WsT* __restrict__ dstw = ws + (size_t)slot * nbuf * W * ld;
     const bool al = ((ld | s0) & 3) == 0;
     const Acc* root = sm + (V >= 2 ? kBYW * kBYSR : 0);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int c = warp + h * kWarpsBY;
-        warp_store_col<Acc, Acc>(dstw + (size_t)(x0 + c) * ld + s0, root + c * kBYSR, rows_out, al, lane);
+        warp_store_col<Acc, WsT>(dstw + (size_t)(x0 + c) * ld + s0, root + c * kBYSR, rows_out, al, lane);
     }
 }
 
@@ -2417,7 +2424,40 @@ int launch_typed(const GroupLaunch& g, cudaStream_t st, LaunchHook hook, void* c
         cudaStreamWaitEvent(to, ev, 0);
     };
     if (both) fork_join(g.ev_fork, st, st1);
-    if (g.nblocks > 0) {
+    bool pass0_done = false;
+    if constexpr (sizeof(Acc) == 8 && std::is_same<Acc, long long>::value && !std::is_same<In, unsigned char>::value) {
+        if (g.k1_acc32) {
+            // pass 0 in int32, block roots widened to int64 on the store
+            // (K1 on the main stream after K1P: two short launches)
+            if (g.nby > 0) {
+                NvtxRange nr("fht: pass 0, width-32 blocks (K1P, int32 -> int64)");
+                auto kb = k1_by32<In, int32_t, 5, kThreadsBYP, long long>;
+                allow_smem(reinterpret_cast<const void*>(kb));
+                dim3 gb((g.H + g.S - 1) / g.S, g.nby, nslots);
+                launch_k(g.pdl, kb, gb, dim3(kThreadsBYP), k1_by32_smem_bytes(), st, reinterpret_cast<const In*>(g.img),
+                         g.img_w, g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.by_x0, ws, g.nbuf,
+                         static_cast<const unsigned char*>(nullptr), 0LL, 0LL, -1LL, -1LL, 0);
+                ++launches;
+                if (hook) hook(ctx, 4);
+            }
+            if (g.nblocks > 0) {
+                NvtxRange nr("fht: pass 0, generic blocks (K1, int32 -> int64)");
+                const size_t smem32 = k1_smem_bytes(kI32, g.k1_max_width, g.k1_sr, g.k1_max_ops, g.k1_max_steps);
+                dim3 g1((g.H + g.S - 1) / g.S, g.nblocks, nslots);
+                auto k1 = k1_blocks<In, int32_t, Out, true, long long>;
+                allow_smem(reinterpret_cast<const void*>(k1));
+                launch_k(g.pdl, k1, g1, dim3(kThreads), smem32, st, reinterpret_cast<const In*>(g.img), g.img_w,
+                         g.img_h, g.img_pitch, g.img_stride, g.img0, g.qs, g.W, g.H, g.ld, g.S, g.blocks, g.shapes,
+                         g.step_offs, g.k1_ops, g.k1_bops, g.k1_max_width, g.k1_sr, g.k1_max_ops, ws, g.nbuf,
+                         g.root_is_block, g.out, static_cast<const unsigned char*>(nullptr), 0LL, 0LL, -1LL, -1LL, 0,
+                         0);
+                ++launches;
+                if (hook) hook(ctx, 1);
+            }
+            pass0_done = true;
+        }
+    }
+    if (!pass0_done && g.nblocks > 0) {
         NvtxRange nr("fht: pass 0, generic blocks (K1)");
         dim3 g1(g.pm_D ? 1 : (g.H + g.S - 1) / g.S, g.nblocks, nslots);
         auto k1 = g.k2_scalar && sizeof(Acc) == 4 ? k1_blocks<In, Acc, Out, true> : k1_blocks<In, Acc, Out, false>;

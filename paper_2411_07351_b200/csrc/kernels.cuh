@@ -114,6 +114,9 @@ struct GroupLaunch {
     // aux stream and events) may be executed by several host threads at
     // once, and a wait must see the record of its own call (std::mutex*)
     void* fork_mu;
+    // int64 plans whose pass-0 sums fit int32 (32 * max|v| < 2^31): K1 and
+    // K1P accumulate in int32 and widen as they store the block roots
+    int k1_acc32 = 0;
     int k1p_variant;    // 5 (default): 4, with levels 1-2 reading the staged u8 columns directly
                         // (no leaf tile) when the input is staged; 4: levels 1-2 in registers,
                         // 3-5 rows interleaved over lanes, the root stored from registers;

@@ -265,7 +265,8 @@ class Plan:
     the reference layout (or (batch, W, H) with layout="native")."""
 
     def __init__(self, width: int, height: int, strategy=SplitStrategy.Tweaked, in_dtype="u8", acc_dtype="i32",
-                 out_dtype=None, quadrants="all", batch: int = 1, layout: str = "reference", device: int = 0):
+                 out_dtype=None, quadrants="all", batch: int = 1, layout: str = "reference", device: int = 0,
+                 pass0_i32: bool = False):
         self.width, self.height, self.batch = int(width), int(height), int(batch)
         self.strategy = _strategy(strategy)
         self.in_dtype = _dtype_code(in_dtype)
@@ -275,7 +276,9 @@ class Plan:
         self.layout = 0 if layout == "reference" else 1
         self.device = int(device)
         h = ctypes.c_void_p()
-        check(lib().fht_plan_create(self.width, self.height, self.strategy, self.in_dtype, self.acc_dtype,
+        # pass0_i32 (acc i64): int32 sums in pass 0, for inputs with 32 * max|v| < 2^31
+        acc_code = self.acc_dtype | 0x100 if pass0_i32 and self.acc_dtype == FHT_I64 else self.acc_dtype
+        check(lib().fht_plan_create(self.width, self.height, self.strategy, self.in_dtype, acc_code,
                                     self.out_dtype, self.mask, self.batch, self.layout, self.device, ctypes.byref(h)))
         self._h = h
         self.workspace_bytes = int(lib().fht_workspace_bytes(h))

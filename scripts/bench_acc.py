@@ -22,11 +22,13 @@ a = ap.parse_args()
 n, b = a.n, a.batch
 sums = 4 * b * n * n * int(np.ceil(np.log2(n)))
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-for in_dt, acc in (("i32", "i32"), ("i64", "i64"), ("i32", "i64"), ("f32", "f32")):
+for in_dt, acc in (("i32", "i32"), ("i64", "i64"), ("i64", "i64p0"), ("i32", "i64"), ("i32", "i64p0"), ("f32", "f32")):
+    p0 = acc == "i64p0"  # int64 plan with pass 0 in int32 (values < 2^20 here: 32 * max|v| < 2^31)
+    acc = "i64" if p0 else acc
     tdt = {"i32": torch.int32, "i64": torch.int64, "f32": torch.float32}[in_dt]
     x = (torch.randint(-(1 << 20), 1 << 20, (b, n, n), dtype=torch.int64) if in_dt != "f32"
          else torch.randn(b, n, n)).to(tdt).cuda()
-    plan = fht.Plan(n, n, "tweaked", in_dtype=in_dt, acc_dtype=acc, batch=b)
+    plan = fht.Plan(n, n, "tweaked", in_dtype=in_dt, acc_dtype=acc, batch=b, pass0_i32=p0)
     out = plan.alloc_outputs()
     for _ in range(3):
         plan(x, out=out)
@@ -55,4 +57,4 @@ for in_dt, acc in (("i32", "i32"), ("i64", "i64"), ("i32", "i64"), ("f32", "f32"
                                      nl, ctypes.byref(got)))
     names = {1: "K1", 5: "stage", 4: "K1P", 2: "K2", 3: "K2root"}
     per = " ".join(f"{names[kind_arr[i]]}={ms_arr[i]:.3f}" for i in range(got.value))
-    print(f"{n}x{n} x{b} in={in_dt} acc={acc}: {m:.4f} ms  {sums / m / 1e6:.1f} Gsums/s  [{per}]")
+    print(f"{n}x{n} x{b} in={in_dt} acc={acc}{' (pass 0 int32)' if p0 else ''}: {m:.4f} ms  {sums / m / 1e6:.1f} Gsums/s  [{per}]")

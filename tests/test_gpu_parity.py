@@ -63,6 +63,41 @@ def test_int64_values_use_int64_accumulation():
         np.testing.assert_array_equal(fht.fht2d(img, s), oracle.fht2d_counted_i64(img, s)[0])
 
 
+@pytest.mark.parametrize("ind", ["i32", "i64"])
+def test_int64_plan_with_int32_pass0(ind):
+    """acc i64 with pass 0 in int32 (FHT_I64_PASS0_I32): values whose full
+    sums need int64 (W * max|v| >= 2^31) but whose width-32 blocks fit int32
+    (32 * max|v| < 2^31) -- identical to the all-int64 plan and the oracle."""
+    rng = np.random.default_rng(12)
+    h, w = 301, 1000
+    imgs = rng.integers(-(1 << 25), 1 << 25, (2, h, w)).astype({"i32": np.int32, "i64": np.int64}[ind])
+    x = torch.from_numpy(imgs).cuda()
+    mixed = fht.Plan(w, h, 1, in_dtype=ind, acc_dtype="i64", batch=2, pass0_i32=True)(x)
+    full = fht.Plan(w, h, 1, in_dtype=ind, acc_dtype="i64", batch=2)(x)
+    torch.cuda.synchronize()
+    for b in range(2):
+        ref, _ = oracle.fht2d_quadrants(imgs[b].astype(np.int64), 1, dtype=np.int64)
+        for k in Q:
+            np.testing.assert_array_equal(mixed[k][b].cpu().numpy(), ref[k])
+            np.testing.assert_array_equal(full[k][b].cpu().numpy(), ref[k])
+
+
+def test_int64_entry_points_choose_int32_pass0():
+    """fht2d_counted / fht2d_quadrants on values in [2^31 / W, 2^26): the
+    entry point picks the int64 plan with pass 0 in int32; bit-exact."""
+    rng = np.random.default_rng(13)
+    img = rng.integers(-(1 << 24), 1 << 24, (257, 700))
+    for s in (0, 1):
+        r = fht.fht2d_counted(img, s)
+        ref, adds = oracle.fht2d_counted_i64(img, s)
+        np.testing.assert_array_equal(r.hough, ref)
+        assert r.additions == adds
+    q = fht.fht2d_quadrants(img, 1)
+    refq, _ = oracle.fht2d_quadrants(img, 1, dtype=np.int64)
+    for k in Q:
+        np.testing.assert_array_equal(getattr(q, k), refq[k])
+
+
 def test_errors_mirror_reference():
     with pytest.raises(fht.OverflowBudget):
         fht.fht2d(np.full((3, 4), 1 << 61, dtype=np.int64))
