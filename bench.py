@@ -288,7 +288,11 @@ def run_ours(args):
     if ws > 1:
         # NCCL across GPUs; FHT_DIST_BACKEND=gloo lets several ranks share one
         # GPU for functional testing (their kernels never wait on each other).
-        backend = os.environ.get("FHT_DIST_BACKEND", "nccl")
+        # More local ranks than GPUs (a functional run on one box) cannot use
+        # NCCL (one rank per device): fall back to gloo for the few host-side
+        # collectives (barrier, timing max); nothing on the data path changes.
+        shared_gpu = int(os.environ.get("LOCAL_WORLD_SIZE", ws)) > torch.cuda.device_count()
+        backend = os.environ.get("FHT_DIST_BACKEND", "gloo" if shared_gpu else "nccl")
         kw = {"device_id": dev} if backend == "nccl" else {}
         dist.init_process_group(backend, init_method="env://", **kw)
     c = workloads.CONFIGS[args.config]
